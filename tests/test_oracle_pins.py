@@ -1,0 +1,402 @@
+"""Pins for the CPU oracle (tests only; SURVEY 8(c) pins P1-P10 + linear-mode pins).
+
+Each test ties the oracle to something other than itself: a textbook value
+(tests/golden/, cited), a closed form, an invariant, or linear-stability
+theory.  A dropped term, a wrong sign, index or constant anywhere in the
+flux / FORCE / update / ghost fill fails at least one of them:
+  * FORCE constants (the 1/2's, dt/dx vs dx/dt)  -> linear density-mode pin
+  * pressure / EOS / energy flux / momentum flux   -> acoustic pin, Sod convergence
+  * conservative update form, periodic wrap        -> conservation pin
+  * reflective wall sign flip                      -> wall conservation pin
+  * sweep direction / transverse momentum handling -> 1-D embedding + 2-D/3-D modes
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    out = {}
+    for line in open(os.path.join(GOLD, name)):
+        line = line.strip()
+        if not line or line.startswith("#"):
+            continue
+        k, v = line.split()
+        out[k] = float(v)
+    return out
+
+
+# ---------------------------------------------------------------- P1: exact Riemann
+def test_p1_sod_star_state_matches_toro():
+    g = _golden("sod_exact_toro.txt")
+    star, _ = oracle.riemann_exact((1.0, 0.0, 1.0), (0.125, 0.0, 0.1), 1.4, [0.0])
+    for got, key in zip(star, ["p_star", "u_star", "rho_star_L", "rho_star_R"]):
+        assert abs(got - g[key]) <= 5e-6 * max(1.0, abs(g[key])) + 5e-6, key
+
+
+def test_p1_sod_wave_positions():
+    g = _golden("sod_exact_toro.txt")
+    t = 0.2
+    x = np.linspace(0.0, 1.0, 200001)
+    _, Wp = oracle.riemann_exact((1.0, 0.0, 1.0), (0.125, 0.0, 0.1), 1.4, (x - 0.5) / t)
+    rho = Wp[:, 0]
+    # shock: last jump in rho; contact: jump from rho*L to rho*R
+    d = np.abs(np.diff(rho))
+    jumps = x[1:][d > 1e-3]
+    assert abs(jumps.max() - g["x_shock"]) < 2e-4
+    assert np.any(np.abs(jumps - g["x_contact"]) < 2e-4)
+    # rarefaction: rho leaves 1 at the head and reaches rho*L at the tail
+    head = x[np.argmax(rho < 1.0 - 1e-9)]
+    tail = x[np.argmax(rho <= g["rho_star_L"] + 1e-9)]
+    assert abs(head - g["x_head"]) < 2e-4
+    assert abs(tail - g["x_tail"]) < 2e-4
+
+
+def test_p1_rankine_hugoniot_across_right_shock():
+    """Mass, momentum and energy fluxes in the shock frame are continuous."""
+    gam = 1.4
+    star, _ = oracle.riemann_exact((1.0, 0.0, 1.0), (0.125, 0.0, 0.1), gam, [0.0])
+    ps, us, _, rsr = star
+    rr, ur, pr = 0.125, 0.0, 0.1
+    S = (rsr * us - rr * ur) / (rsr - rr)  # from mass conservation
+    g = _golden("sod_exact_toro.txt")
+    assert abs(S - g["shock_speed"]) < 1e-5
+    mom = lambda r, u, p: r * (u - S) ** 2 + p
+    ene = lambda r, u, p: (u - S) * (p / (gam - 1) + 0.5 * r * (u - S) ** 2 + p)
+    assert abs(mom(rsr, us, ps) - mom(rr, ur, pr)) < 1e-12
+    assert abs(ene(rsr, us, ps) - ene(rr, ur, pr)) < 1e-12
+
+
+# ---------------------------------------------------------------- P2: Sod convergence
+def _sod_l1(N):
+    grid = oracle.Grid((N,), pad=2)
+    U, nsteps = oracle.run_cfl(grid, W.sod(N), 0.2, cfl=0.9, n_reduced=5, reduce=0.2)
+    x = (np.arange(N) + 0.5) / N
+    _, Wx = oracle.riemann_exact((1.0, 0.0, 1.0), (0.125, 0.0, 0.1), 1.4, (x - 0.5) / 0.2)
+    return np.sum(np.abs(U[:, 0] - Wx[:, 0])) / N, nsteps
+
+
+def test_p2_sod_converges_at_first_order_rate():
+    Ns = [100, 200, 400, 800, 1600]
+    errs = []
+    for N in Ns:
+        e, n = _sod_l1(N)
+        errs.append(e)
+        if N == 200:
+            assert n == 100
+            assert abs(e - 1.45e-2) <= 0.1 * 1.45e-2
+    errs = np.array(errs)
+    assert np.all(np.diff(errs) < 0), errs
+    rates = np.log2(errs[:-1] / errs[1:])
+    assert np.all((rates >= 0.5) & (rates <= 1.0)), rates
+
+
+# ---------------------------------------------------------------- P3: smooth order 1
+def test_p3_smooth_wave_order_one():
+    errs = []
+    Ns = [100, 200, 400, 800]
+    for N in Ns:
+        grid = oracle.Grid((N,), pad=2, bc_lo=[oracle.BC_PERIODIC], bc_hi=[oracle.BC_PERIODIC])
+        U0 = W.smooth_density_wave((N,), vel=[1.0])
+        c = math.sqrt(1.4)
+        nsteps = int(math.ceil(1.0 / (0.5 / N / (1.0 + c))))
+        dt = 1.0 / nsteps
+        U = oracle.step(grid, U0, dt, nsteps)
+        # exact: translation by u*t = 1 (one period) -> initial profile
+        errs.append(np.sum(np.abs(U[:, 0] - U0[:, 0])) / N)
+    rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert rates[-1] >= 0.9 and rates[-2] >= 0.9, rates
+
+
+# ---------------------------------------------------------------- linear density mode
+def _force_g(theta, c):
+    """Amplification of FORCE for linear advection:
+    g = 1 - i c sin(theta) - (1 + c^2)/2 (1 - cos(theta))."""
+    return 1.0 - 1j * c * np.sin(theta) - 0.5 * (1.0 + c * c) * (1.0 - np.cos(theta))
+
+
+@pytest.mark.parametrize("n,vel,k", [((64,), [0.7], [3]),
+                                     ((32, 24), [0.6, -0.45], [2, 3]),
+                                     ((16, 12, 10), [0.5, 0.3, -0.4], [1, 2, 3])])
+def test_density_mode_amplification_exact(n, vel, k):
+    """A density wave at constant u, p is an exact invariant manifold of the Euler
+    equations on which F(U) = u U + const; FORCE then reduces to the linear FORCE
+    scheme, and each split sweep multiplies the Fourier mode by g(theta_d, c_d)."""
+    D = len(n)
+    per = [oracle.BC_PERIODIC] * D
+    grid = oracle.Grid(n, pad=2, bc_lo=per, bc_hi=per)
+    U0 = W.smooth_density_wave(n, vel=vel, amp=0.2, k=k)
+    dt = 0.37 / max(n)
+    nsteps = 7
+    U = oracle.step(grid, U0, dt, nsteps)
+    d0 = np.fft.fftn(U0[..., 0] - 1.0)
+    d1 = np.fft.fftn(U[..., 0] - 1.0)
+    gtot = 1.0 + 0j
+    for d in range(D):
+        theta = 2 * math.pi * k[d] / n[d]
+        gtot *= _force_g(theta, vel[d] * dt / grid.dx[d])
+    idx = tuple([(-k[d]) % n[d] for d in reversed(range(D))])  # sin has +/- k modes
+    idx2 = tuple([k[d] % n[d] for d in reversed(range(D))])
+    # numpy axis order is (z, y, x); k[d] belongs to axis D-1-d
+    want = d0[idx2] * gtot ** nsteps
+    assert abs(d1[idx2] - want) <= 1e-12 * abs(d0[idx2])
+    assert abs(d1[idx] - d0[idx] * np.conj(gtot) ** nsteps) <= 1e-12 * abs(d0[idx])
+    # all other modes stay zero
+    mask = np.ones(d1.shape, bool)
+    mask[idx] = mask[idx2] = False
+    assert np.max(np.abs(d1[mask])) <= 1e-11 * abs(d0[idx2])
+
+
+# ---------------------------------------------------------------- acoustic (linearised) pin
+def _jacobian(U, d, gamma):
+    """Textbook flux Jacobian dF_d/dU of the Euler equations in conserved variables."""
+    D = len(U) - 2
+    rho, m, E = U[0], U[1:1 + D], U[-1]
+    u = m / rho
+    q2 = float(u @ u)
+    p = (gamma - 1) * (E - 0.5 * rho * q2)
+    H = (E + p) / rho
+    g1 = gamma - 1
+    A = np.zeros((D + 2, D + 2))
+    A[0, 1 + d] = 1.0
+    for k in range(D):
+        A[1 + k, 0] = -u[k] * u[d] + (g1 * q2 / 2 if k == d else 0.0)
+        for j in range(D):
+            A[1 + k, 1 + j] = (u[d] if k == j else 0.0) + (u[k] if j == d else 0.0) \
+                - (g1 * u[j] if k == d else 0.0)
+        A[1 + k, -1] = g1 if k == d else 0.0
+    A[-1, 0] = u[d] * (g1 * q2 / 2 - H)
+    for j in range(D):
+        A[-1, 1 + j] = (H if j == d else 0.0) - g1 * u[j] * u[d]
+    A[-1, -1] = gamma * u[d]
+    return A
+
+
+def _base_state(D):
+    rho, p = 1.1, 0.9
+    u = np.array([0.3, -0.2, 0.15][:D])
+    return np.concatenate([[rho], rho * u, [p / 0.4 + 0.5 * rho * u @ u]]), u, rho, p
+
+
+@pytest.mark.parametrize("D", [1, 2, 3])
+def test_jacobian_eigenvalues_are_wave_speeds(D):
+    """Pins the Jacobian used by the acoustic test: eig(A_d) = u_d - c, u_d (x D), u_d + c."""
+    U, u, rho, p = _base_state(D)
+    c = math.sqrt(1.4 * p / rho)
+    for d in range(D):
+        ev = np.sort(np.linalg.eigvals(_jacobian(U, d, 1.4)).real)
+        want = np.sort([u[d] - c] + [u[d]] * D + [u[d] + c])
+        assert np.allclose(ev, want, atol=1e-12)
+
+
+@pytest.mark.parametrize("n", [(48,), (16, 12)])
+def test_acoustic_perturbation_follows_linear_force(n):
+    """Small random perturbation of a uniform state (periodic) evolves, to O(eps^2),
+    by the linear FORCE amplification matrices of the Euler Jacobians, applied per
+    split sweep: G_d(theta) = I - i lam A_d sin(theta) - 1/2 (I + lam^2 A_d^2)(1 - cos(theta))."""
+    D = len(n)
+    U0, u, rho, p = _base_state(D)
+    per = [oracle.BC_PERIODIC] * D
+    grid = oracle.Grid(n, pad=2, bc_lo=per, bc_hi=per)
+    eps = 1e-6
+    rng_pert = np.stack([W.uniform_pm1(7, s, np.arange(int(np.prod(n)))).reshape(
+        tuple(reversed(n))) for s in range(D + 2)], axis=-1)
+    Ustate = U0 + eps * rng_pert
+    dt = 0.3 / max(n)
+    nsteps = 5
+    Uout = oracle.step(grid, Ustate, dt, nsteps)
+    dU_num = Uout - U0
+    # linear prediction in Fourier space
+    dhat = np.fft.fftn(eps * rng_pert, axes=tuple(range(D)))
+    C = D + 2
+    A = [_jacobian(U0, d, 1.4) for d in range(D)]
+    shape = tuple(reversed(n))
+    for idx in np.ndindex(*shape):
+        G = np.eye(C, dtype=complex)
+        for d in range(D):
+            kd = idx[D - 1 - d]
+            th = 2 * math.pi * kd / n[d]
+            lam = dt / grid.dx[d]
+            Gd = np.eye(C) - 1j * lam * A[d] * math.sin(th) \
+                - 0.5 * (np.eye(C) + lam * lam * A[d] @ A[d]) * (1 - math.cos(th))
+            G = Gd @ G  # x sweep first, then y (Listing 8 order)
+        dhat[idx] = np.linalg.matrix_power(G, nsteps) @ dhat[idx]
+    dU_lin = np.fft.ifftn(dhat, axes=tuple(range(D))).real
+    err = np.max(np.abs(dU_num - dU_lin))
+    assert err <= 1e-4 * np.max(np.abs(dU_lin)), err
+
+
+# ---------------------------------------------------------------- P4: uniform state
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("n", [(17,), (9, 7), (5, 6, 4)])
+@pytest.mark.parametrize("bc", [oracle.BC_TRANSMISSIVE, oracle.BC_PERIODIC])
+def test_p4_uniform_state_bitwise(dtype, n, bc):
+    D = len(n)
+    grid = oracle.Grid(n, pad=2, bc_lo=[bc] * D, bc_hi=[bc] * D)
+    U0 = W.uniform(n, rho=0.8, vel=[0.3, -0.7, 0.2][:D], p=1.3).astype(dtype)
+    U = oracle.step(grid, U0, 0.01, 5)
+    assert np.array_equal(U, U0)
+
+
+# ---------------------------------------------------------------- P5: conservation
+@pytest.mark.parametrize("n,dtype,tol", [((40, 24), np.float64, 1e-13),
+                                         ((10, 8, 6), np.float64, 1e-13),
+                                         ((40, 24), np.float32, 1e-5)])
+def test_p5_periodic_conservation(n, dtype, tol):
+    D = len(n)
+    per = [oracle.BC_PERIODIC] * D
+    grid = oracle.Grid(n, pad=2, bc_lo=per, bc_hi=per)
+    U0 = W.random_state(n).astype(dtype)
+    S = oracle.max_wavespeed(grid, U0)
+    dt = 0.4 * min(grid.dx) / S
+    U = oracle.step(grid, U0, dt, 100)
+    s0 = np.array([math.fsum(U0[..., c].astype(np.float64).ravel()) for c in range(D + 2)])
+    s1 = np.array([math.fsum(U[..., c].astype(np.float64).ravel()) for c in range(D + 2)])
+    scale = np.array([math.fsum(np.abs(U0[..., c].astype(np.float64)).ravel())
+                      for c in range(D + 2)])
+    assert np.all(np.abs(s1 - s0) <= tol * scale), (s1 - s0) / scale
+    assert not np.array_equal(U, U0)
+
+
+def test_reflective_walls_conserve_mass_and_energy():
+    """At a reflective wall the FORCE mass and energy fluxes vanish exactly
+    (mirror state, normal momentum negated), so rho and E are conserved."""
+    n = (30, 20)
+    refl = [oracle.BC_REFLECTIVE] * 2
+    grid = oracle.Grid(n, pad=2, bc_lo=refl, bc_hi=refl)
+    U0 = W.random_state(n)
+    dt = 0.4 * min(grid.dx) / oracle.max_wavespeed(grid, U0)
+    U = oracle.step(grid, U0, dt, 50)
+    for c in (0, 3):
+        s0, s1 = math.fsum(U0[..., c].ravel()), math.fsum(U[..., c].ravel())
+        assert abs(s1 - s0) <= 1e-13 * abs(s0)
+    # momentum is NOT conserved (wall pressure force): the pin is not vacuous
+    assert abs(math.fsum(U[..., 1].ravel()) - math.fsum(U0[..., 1].ravel())) > 1e-6
+
+
+# ---------------------------------------------------------------- P6 / P7: symmetry, embedding
+def test_p6_mirrored_sod_is_mirrored_bitwise():
+    N = 100
+    grid = oracle.Grid((N,), pad=2)
+    U = W.sod(N)
+    Um = U[::-1].copy()
+    Um[:, 1] = -Um[:, 1]
+    dt = 0.5 / N / 2.5
+    A = oracle.step(grid, U, dt, 40)
+    B = oracle.step(grid, Um, dt, 40)
+    Bm = B[::-1].copy()
+    Bm[:, 1] = -Bm[:, 1]
+    assert np.array_equal(A, Bm)
+
+
+@pytest.mark.parametrize("n,axis", [((40, 6), 0), ((6, 40), 1), ((5, 40, 4), 1),
+                                    ((4, 5, 40), 2), ((40, 3, 4), 0)])
+def test_p7_embedded_sod_equals_1d_bitwise(n, axis):
+    D = len(n)
+    N = n[axis]
+    dx = [1.0 / N] * D
+    grid = oracle.Grid(n, pad=2, dx=dx)
+    g1 = oracle.Grid((N,), pad=2, dx=[1.0 / N])
+    dt = 0.5 / N / 2.5
+    U = oracle.step(grid, W.sod_embedded(n, axis), dt, 30)
+    u1 = oracle.step(g1, W.sod(N), dt, 30)
+    # move the sweep axis to the last numpy axis, compare every line
+    lines = np.moveaxis(U, D - 1 - axis, D - 1).reshape(-1, N, D + 2)
+    for line in lines:
+        assert np.array_equal(line[:, 0], u1[:, 0])
+        assert np.array_equal(line[:, 1 + axis], u1[:, 1])
+        assert np.array_equal(line[:, -1], u1[:, 2])
+        others = [1 + k for k in range(D) if k != axis]
+        assert np.all(line[:, others] == 0.0)
+
+
+# ---------------------------------------------------------------- ghost fill (set_boundary)
+def test_ghost_fill_examples_spec():
+    """Clamp on [a, b, c] with pad 1 -> [a | a b c | c]; periodic wraps;
+    reflective mirrors with the normal momentum negated."""
+    vals = np.array([[1.0, 10.0, 5.0], [2.0, 20.0, 6.0], [3.0, 30.0, 7.0]])
+    for bc, lo, hi in [(oracle.BC_TRANSMISSIVE, vals[0], vals[2]),
+                       (oracle.BC_PERIODIC, vals[2], vals[0]),
+                       (oracle.BC_REFLECTIVE, vals[0] * [1, -1, 1], vals[2] * [1, -1, 1])]:
+        g = oracle.Grid((3,), pad=1, bc_lo=[bc], bc_hi=[bc])
+        P = np.zeros((5, 3))
+        P[1:4] = vals
+        P = oracle.fill_ghosts(g, P)
+        assert np.array_equal(P[0], lo) and np.array_equal(P[4], hi)
+        assert np.array_equal(P[1:4], vals)
+
+
+def test_ghost_fill_pad2_layers_and_corners():
+    n = (4, 3)
+    bcs_lo = [oracle.BC_REFLECTIVE, oracle.BC_PERIODIC]
+    bcs_hi = [oracle.BC_TRANSMISSIVE, oracle.BC_PERIODIC]
+    g = oracle.Grid(n, pad=2, bc_lo=bcs_lo, bc_hi=bcs_hi)
+    interior = W.random_state(n)
+    P = np.zeros(oracle.padded_shape(g))
+    P[2:5, 2:6] = interior
+    P = oracle.fill_ghosts(g, P)
+
+    def src(i, N, lo, hi):
+        if 0 <= i < N:
+            return i, False
+        kind = lo if i < 0 else hi
+        if kind == oracle.BC_TRANSMISSIVE:
+            return (0 if i < 0 else N - 1), False
+        if kind == oracle.BC_PERIODIC:
+            return i % N, False
+        return (-1 - i if i < 0 else 2 * N - 1 - i), True
+
+    for j in range(-2, 5):
+        for i in range(-2, 6):
+            si, fx = src(i, 4, bcs_lo[0], bcs_hi[0])
+            sj, fy = src(j, 3, bcs_lo[1], bcs_hi[1])
+            want = interior[sj, si].copy()
+            if fx:
+                want[1] = -want[1]
+            if fy:
+                want[2] = -want[2]
+            assert np.array_equal(P[j + 2, i + 2], want), (i, j)
+
+
+# ---------------------------------------------------------------- max wavespeed
+def test_max_wavespeed_closed_form():
+    n = (6, 5)
+    g = oracle.Grid(n)
+    U = W.uniform(n, rho=2.0, vel=[0.6, -0.8], p=3.0)
+    assert abs(oracle.max_wavespeed(g, U) - (1.0 + math.sqrt(1.4 * 3.0 / 2.0))) < 1e-14
+    gold = _golden("mach381_shock.txt")
+    r2, u2, p2 = W.mach_shock_state()
+    assert abs(r2 - gold["rho2"]) < 1e-5 and abs(u2 - gold["u2"]) < 1e-5
+    assert abs(p2 - gold["p2"]) < 1e-5
+    sb = W.shock_bubble((64, 64), perturb=0.0)
+    assert abs(oracle.max_wavespeed(oracle.Grid((64, 64)), sb) - gold["max_wavespeed"]) < 1e-4
+
+
+def test_domain_error_on_negative_pressure():
+    n = (8,)
+    g = oracle.Grid(n)
+    U = W.uniform(n)
+    U[:, 2] = -1.0  # E < 0 -> p < 0 everywhere
+    with pytest.raises(oracle.DomainError):
+        oracle.step(g, U, 0.01, 1)
+
+
+def test_fp32_tracks_fp64_on_shock_bubble():
+    """fp32 oracle is the same scheme at lower precision (reading S16)."""
+    n = (64, 48)
+    g = oracle.Grid(n, dx=[1 / 64] * 2)
+    U0 = W.shock_bubble(n, dx=[1 / 64] * 2)
+    dt = 0.4 / 64 / oracle.max_wavespeed(g, U0)
+    a = oracle.step(g, U0, dt, 20)
+    b = oracle.step(g, U0.astype(np.float32), dt, 20)
+    err = np.max(np.abs(a - b), axis=(0, 1))
+    scale = np.max(np.abs(a), axis=(0, 1))
+    scale[2] = scale[1]  # m_y is a tiny perturbation-driven field: measure against |m|
+    assert np.all(err / scale < 1e-5), err / scale
