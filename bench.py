@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the split FORCE step (Ripple, arXiv 2104.08571) on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                    [--workload 2d1024|s512|w384|l256] [--kernel fused|split]
+
+Metric (BASELINE.json): Gcell-updates/s = global interior cells x steps / time / 1e9,
+plus the HBM-roofline fraction of the dominant kernel.
+
+Default workload = BASELINE.json configs[1]: 2-D Euler, 1024 x 1024 cells per GPU,
+pad 2, fp64, SoA, shock-bubble initial data (workloads.shock_bubble), fixed
+dt = 0.4 dx / S0.  At N > 1 (torchrun, one process per GPU, NCCL) the grid grows
+in y (1024 x 1024N, y-split into N partitions: the paper's weak-scaling setup,
+P:1393-1402) -> "scaling": "weak".  The two 33.5 MB state buffers fit in the
+126 MB L2, so L2 is flushed (256 MiB write) between timed steps and each step is
+timed with its own CUDA events on the library's stream (flush excluded).
+
+Only the --impl reference leg and the cpu_baseline object execute oracle/ (the
+plain-C CPU oracle, timed as a reported baseline, never the product path).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: ndim, per-GPU (weak) or global (strong) size, dtype, scaling, config label
+    "2d1024": dict(ndim=2, n=(1024, 1024), dtype="f64", scaling="weak",
+                   label="2-D Euler FORCE 1024x1024/GPU pad 2 fp64 (BASELINE configs[1])"),
+    "s512": dict(ndim=3, n=(512, 512, 512), dtype="f64", scaling="strong",
+                 label="3-D Euler FORCE 512^3 fp64 z-slabs (BASELINE configs[2])"),
+    "w384": dict(ndim=3, n=(384, 384, 384), dtype="f32", scaling="weak",
+                 label="3-D Euler FORCE 384^3/GPU fp32 blocks (BASELINE configs[3])"),
+    "l256": dict(ndim=3, n=(256, 256, 256), dtype="f32", scaling="weak",
+                 label="3-D Euler FORCE 256^3 (BASELINE configs[4])"),
+}
+W384_BLOCKS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+
+
+def decomposition(wl, nranks):
+    """Global size and partition grid for N ranks."""
+    n = list(wl["n"])
+    D = wl["ndim"]
+    if wl["scaling"] == "strong":
+        parts = [1] * D
+        parts[D - 1] = nranks
+        return n, parts
+    if D == 3 and nranks in W384_BLOCKS:
+        parts = list(W384_BLOCKS[nranks])
+    else:
+        parts = [1] * D
+        parts[D - 1] = nranks
+    return [n[d] * parts[d] for d in range(D)], parts
+
+
+class Clocks:
+    """Sample nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout
+                f = [v.strip() for v in out.strip().split(",")]
+                if len(f) >= 7:
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(key):
+    """dram bytes read+write per launch of the dominant kernel, from the committed
+    ncu --set full capture summary (profiles/ncu_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+def cpu_baseline(wl, steps_cap=60, budget_s=12.0):
+    """The oracle as it stands (plain C, 1 thread) on a bounded sample of the workload."""
+    import numpy as np  # noqa
+
+    import oracle
+    import workloads as W
+    D = wl["ndim"]
+    n = list(wl["n"])
+    if D == 3:  # bounded sample: a 128^3 sub-box of the same recipe
+        n = [128, 128, 128]
+    dx = [1.0 / wl["n"][0]] * D
+    U = W.shock_bubble(tuple(n), dx=dx)
+    if wl["dtype"] == "f32":
+        U = U.astype(np.float32)
+    g = oracle.Grid(tuple(n), pad=2, dx=dx)
+    dt = 0.4 * dx[0] / oracle.max_wavespeed(g, U.astype(np.float64))
+    t0 = time.perf_counter()
+    oracle.step(g, U, dt, 1)
+    one = time.perf_counter() - t0
+    k = max(1, min(steps_cap, int(budget_s / max(one, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.step(g, U, dt, k)
+    el = time.perf_counter() - t0
+    cells = int(np.prod(n))
+    return {"value": cells * k / el / 1e9, "unit": "Gcell-updates/s", "cores": 1,
+            "kind": "oracle",
+            "sample": f"{'x'.join(map(str, n))} shock-bubble {wl['dtype']}, {k} steps, "
+                      f"plain-C oracle single thread ({el:.1f} s)"}
+
+
+def run_reference(args, wl):
+    """--impl reference: the oracle on this arm's config/metric (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+    import workloads as W
+    D = wl["ndim"]
+    n = list(wl["n"])
+    full = int(np.prod(n))
+    sample_n = n if full <= 2 ** 20 else [min(v, 128) for v in n]
+    dx = [1.0 / n[0]] * D
+    U = W.shock_bubble(tuple(sample_n), dx=dx)
+    if wl["dtype"] == "f32":
+        U = U.astype(np.float32)
+    g = oracle.Grid(tuple(sample_n), pad=2, dx=dx)
+    dt = 0.4 * dx[0] / oracle.max_wavespeed(g, U.astype(np.float64))
+    for _ in range(args.warmup):
+        U = oracle.step(g, U, dt, 1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        U = oracle.step(g, U, dt, 1)
+    el = time.perf_counter() - t0
+    cells = int(np.prod(sample_n))
+    value = cells * args.steps / el / 1e9
+    sample = (f"{'x'.join(map(str, sample_n))} of the workload per step "
+              f"({'full grid' if sample_n == n else 'sub-box'}), plain-C oracle, 1 thread")
+    line = {"impl": "reference", "metric": "Gcell-updates/s", "value": value,
+            "unit": "Gcell-updates/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
+            "dtype": wl["dtype"], "data": "synthetic",
+            "config": {"workload": wl["label"], "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "Gcell-updates/s", "cores": 1,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "Gcell-updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="2d1024", choices=sorted(WORKLOADS))
+    ap.add_argument("--kernel", default="fused", choices=["fused", "split"])
+    ap.add_argument("--rows", type=int, default=0, help="rows per warp task (0 = auto)")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_08571_b200 as R
+    import workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    stream = torch.cuda.current_stream()
+
+    gn, parts = decomposition(wl, world)
+    D = wl["ndim"]
+    dx = [1.0 / wl["n"][0]] * D
+    nccl_id = None
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(R.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
+    dom = R.Domain(gn, pad=2, parts=parts, dtype=wl["dtype"], kernel=args.kernel, dx=dx,
+                   nranks=world, rank=rank if world > 1 else 0, nccl_id=nccl_id, device=dev,
+                   stream=stream.cuda_stream, rows_per_chunk=args.rows)
+    box = (dom.lo, dom.hi)
+    U0 = W.shock_bubble(tuple(gn), dx=dx, box=box)
+    if wl["dtype"] == "f32":
+        U0 = U0.astype(np.float32)
+    dom.set_state(U0)
+    S0 = dom.max_wavespeed()
+    dt = 0.4 * min(dx) / S0
+    local_cells = int(np.prod([dom.box[d] for d in range(D)]))
+    global_cells = int(np.prod(gn))
+    elem = 8 if wl["dtype"] == "f64" else 4
+    C = D + 2
+
+    flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def do_flush():
+        if flush is not None:
+            flush.fill_(1)
+
+    for _ in range(args.warmup):
+        dom.advance(dt, 1)
+        do_flush()
+    torch.cuda.synchronize()
+
+    launches_per_step = dom.launches_per_step
+    dom.profile(args.steps * 64)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    with Clocks(dev) as clk:
+        for k in range(args.steps):
+            ev[k][0].record(stream)
+            dom.advance(dt, 1)
+            ev[k][1].record(stream)
+            do_flush()
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    kern_ms, kern_launches = dom.profile_read()
+    dom.profile(0)
+    t_total = sum(step_ms) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_total = float(tt.item())
+    dom.synchronize()  # surfaces any domain error of the timed steps
+
+    # ---- e2e through the public API with host buffers (pinned), copies timed
+    e2e = None
+    if args.e2e_steps > 0:
+        tdt = torch.float64 if elem == 8 else torch.float32
+        h_in = torch.empty(C * local_cells, dtype=tdt, pin_memory=True)
+        h_out = torch.empty(C * local_cells, dtype=tdt, pin_memory=True)
+        h_in.numpy()[:] = np.ascontiguousarray(np.moveaxis(U0, -1, 0)).ravel()
+        dom.get_state_ptr(h_out.data_ptr())
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            dom.set_state_ptr(h_in.data_ptr())
+            dom.advance(dt, 1)
+            dom.get_state_ptr(h_out.data_ptr())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = e0.elapsed_time(e1) / 1e3
+        if world > 1:
+            tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        nb = C * local_cells * elem
+        e2e = {"value": global_cells * args.e2e_steps / te / 1e9, "unit": "Gcell-updates/s",
+               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "steps": args.e2e_steps,
+               "path": "rpl_set_state(pinned host) + rpl_advance(dt,1) + rpl_get_state(pinned host)"}
+
+    value = global_cells * args.steps / t_total / 1e9
+    peak, peak_src = measured_peak_gbs()
+    alg_bytes = 2 * C * elem * local_cells  # per step-kernel launch (one partition per rank)
+    kname = {"fused": "k_step2d" if D == 2 else "k_sweep", "split": "k_sweep"}[args.kernel]
+    per_launch_ms = kern_ms / max(kern_launches, 1)
+    launches_per_step_kernel = max(1, kern_launches // args.steps)
+    if args.kernel == "split" or D != 2:
+        alg_bytes_launch = alg_bytes  # each sweep reads+writes the state once
+    else:
+        alg_bytes_launch = alg_bytes
+    achieved = alg_bytes_launch / (per_launch_ms / 1e3) / 1e9
+    traffic = ncu_traffic(f"{args.workload}_{args.kernel}")
+    roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+            "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json copy bandwidth, burst)",
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "alg_bytes_per_launch": alg_bytes_launch, "launch_ms": per_launch_ms,
+            "launches_per_step": launches_per_step_kernel,
+            "frac_of_8TBs": achieved / 8000.0}
+    line = {"metric": "Gcell-updates/s", "value": value, "unit": "Gcell-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True,
+            "scaling": wl["scaling"], "vs_baseline": None, "dtype": wl["dtype"],
+            "data": "synthetic",
+            "config": {"workload": wl["label"], "global_cells": gn, "parts": parts,
+                       "kernel": args.kernel, "layout": "soa",
+                       "l2": "flushed between steps (256 MiB write), per-step CUDA events"
+                             if flush is not None else "not flushed",
+                       "timing": "sum of per-step CUDA events on the library stream, max over ranks",
+                       "wall_s": wall, "dt": dt, "S0": S0},
+            "roofline": roof, "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary()}
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dom.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,27 @@
+// kernels.hpp -- host-side launch entry points of kernels.cu (no torch types).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "geometry.hpp"
+
+namespace rpl {
+
+template <typename T>
+struct KArgs;
+
+template <typename T>
+void launch_sweep(const KArgs<T>& a, int d, cudaStream_t s);      // K-A, one launch
+template <typename T>
+void launch_step2d(const KArgs<T>& a, cudaStream_t s);            // K-B 2-D, one launch
+template <typename T>
+void launch_step3d(const KArgs<T>& a, cudaStream_t s);            // K-B 3-D, one launch
+template <typename T>
+void launch_fill(const Geom& g, int part, T* const* bufs, cudaStream_t s);
+template <typename T>
+void launch_maxws(const Geom& g, const T* in, double gamma, unsigned long long* smax,
+                  unsigned* flag, cudaStream_t s);
+
+int auto_rows_2d(const Geom& g);
+int auto_rows_3d(const Geom& g);
+
+}  // namespace rpl

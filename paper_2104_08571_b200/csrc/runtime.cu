@@ -1,0 +1,794 @@
+// runtime.cu -- the rpl_* C ABI (include/ripple_fv.h): domain lifetime, state
+// transfer, padding fill, the step pipeline, the wavespeed reduction and the
+// NCCL halo exchange.  One process per GPU; all device work is enqueued on one
+// stream (the caller's, e.g. torch's current stream) in the order of Listing 8
+// (P:1340-1358); no host synchronisation inside rpl_advance on one rank.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ripple_fv.h"
+#include "geometry.hpp"
+#include "kernels.hpp"
+#include "plan.hpp"
+#include "scheme.cuh"
+
+using namespace rpl;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+static rpl_status fail(rpl_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CU(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(RPL_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                  \
+  } while (0)
+
+extern "C" const char* rpl_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+// NCCL is resolved at run time from the libnccl.so.2 already loaded in the
+// process (torch's), else from the loader path: the library has no link-time
+// NCCL dependency and single-rank use never touches it.
+namespace {
+struct Nccl {
+  bool tried = false, ok = false;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  bool load() {
+    if (tried) return ok;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) {
+      const char* env = getenv("RPL_NCCL_LIB");
+      h = dlopen(env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) return false;
+#define RPL_SYM(n) n = (decltype(n))dlsym(h, "nccl" #n)
+    RPL_SYM(GetUniqueId);
+    RPL_SYM(CommInitRank);
+    RPL_SYM(CommDestroy);
+    RPL_SYM(Send);
+    RPL_SYM(Recv);
+    RPL_SYM(GroupStart);
+    RPL_SYM(GroupEnd);
+    RPL_SYM(AllReduce);
+    RPL_SYM(GetErrorString);
+#undef RPL_SYM
+    ok = GetUniqueId && CommInitRank && CommDestroy && Send && Recv && GroupStart && GroupEnd &&
+         AllReduce && GetErrorString;
+    return ok;
+  }
+} g_nccl;
+}  // namespace
+
+#define NC(call)                                                                           \
+  do {                                                                                     \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      return fail(RPL_E_NCCL, "%s failed: %s", #call, g_nccl.GetErrorString(r_));         \
+  } while (0)
+
+// ------------------------------------------------------------------ small kernels
+namespace {
+
+struct DevEdge {
+  int64_t src_lo[3], src_hi[3], dst_lo[3], dst_hi[3];
+  int mode[3];
+  int src_part, dst_part;
+  int64_t count;   // cells in the dst box
+  int64_t offset;  // element offset of this edge's message in the peer buffer
+};
+
+// pack (dir 0): message[c][i] = source cell of dst-box cell i (flips applied)
+// unpack (dir 1): ghost cell i of dst <- message[c][i]
+template <typename T, int D, int L>
+__global__ void k_edge(const Geom g, const DevEdge e, T* buf, T* msg, int dir) {
+  const int64_t ex = e.dst_hi[0] - e.dst_lo[0], ey = e.dst_hi[1] - e.dst_lo[1];
+  int pcs[3], pcd[3];
+  g.part_coords(e.src_part, pcs);
+  g.part_coords(e.dst_part, pcd);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e.count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t[3] = {e.dst_lo[0] + i % ex, e.dst_lo[1] + (i / ex) % ey,
+                          e.dst_lo[2] + i / (ex * ey)};
+    T v[D + 2];
+    if (dir == 0) {
+      int64_t s[3];
+      bool flip[3] = {false, false, false};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int64_t k = t[d] - e.dst_lo[d];
+        s[d] = e.mode[d] == RPL_MAP_TRANSLATE ? e.src_lo[d] + k
+               : e.mode[d] == RPL_MAP_REFLECT ? e.src_hi[d] - 1 - k
+                                              : e.src_lo[d];
+        flip[d] = e.mode[d] == RPL_MAP_REFLECT;
+        s[d] -= (d < D) ? (int64_t)pcs[d] * g.S[d] : 0;
+      }
+#pragma unroll
+      for (int c = 0; c < D + 2; ++c) {
+        const int64_t j = L == 0 ? c * g.comp_stride + g.row(s[1], s[2]) * g.pitch + g.xo + s[0]
+                                 : (g.row(s[1], s[2]) * g.pitch + g.xo + s[0]) * (D + 2) + c;
+        v[c] = buf[j];
+      }
+#pragma unroll
+      for (int d = 0; d < D; ++d)
+        if (flip[d]) v[1 + d] = -v[1 + d];
+#pragma unroll
+      for (int c = 0; c < D + 2; ++c) msg[c * e.count + i] = v[c];
+    } else {
+      int64_t l[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) l[d] = t[d] - ((d < D) ? (int64_t)pcd[d] * g.S[d] : 0);
+#pragma unroll
+      for (int c = 0; c < D + 2; ++c) v[c] = msg[c * e.count + i];
+      store_cell<D, L>(g, buf, l[0], l[1], l[2], v);
+    }
+  }
+}
+
+// interior <-> dense SoA staging [C][S2][S1][S0] (AoS layout transfers)
+template <typename T, int D>
+__global__ void k_stage(const Geom g, T* buf, T* stage, int dir) {
+  const int64_t n = g.cells();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = i % g.S[0], y = (i / g.S[0]) % g.S[1], z = i / (g.S[0] * g.S[1]);
+#pragma unroll
+    for (int c = 0; c < D + 2; ++c) {
+      const int64_t j = (g.row(y, z) * g.pitch + g.xo + x) * (D + 2) + c;
+      if (dir == 0) buf[j] = stage[c * n + i];
+      else stage[c * n + i] = buf[j];
+    }
+  }
+}
+
+template <typename T>
+void launch_edge(const Geom& g, const DevEdge& e, T* buf, T* msg, int dir, cudaStream_t s) {
+  int grid = (int)((e.count + 255) / 256);
+  if (grid > 148 * 8) grid = 148 * 8;
+  if (grid < 1) grid = 1;
+#define RPL_E(DD, LL) k_edge<T, DD, LL><<<grid, 256, 0, s>>>(g, e, buf, msg, dir)
+  if (g.D == 1) { if (g.layout == 0) RPL_E(1, 0); else RPL_E(1, 1); }
+  if (g.D == 2) { if (g.layout == 0) RPL_E(2, 0); else RPL_E(2, 1); }
+  if (g.D == 3) { if (g.layout == 0) RPL_E(3, 0); else RPL_E(3, 1); }
+#undef RPL_E
+}
+
+template <typename T>
+void launch_stage(const Geom& g, T* buf, T* stage, int dir, cudaStream_t s) {
+  int grid = (int)((g.cells() + 255) / 256);
+  if (grid > 148 * 8) grid = 148 * 8;
+  if (g.D == 1) k_stage<T, 1><<<grid, 256, 0, s>>>(g, buf, stage, dir);
+  if (g.D == 2) k_stage<T, 2><<<grid, 256, 0, s>>>(g, buf, stage, dir);
+  if (g.D == 3) k_stage<T, 3><<<grid, 256, 0, s>>>(g, buf, stage, dir);
+}
+
+struct Peer {
+  int rank;
+  std::vector<DevEdge> edges;  // edges of this peer, in plan order
+  int64_t elems = 0;           // message elements
+  int64_t offset = 0;          // offset into the send/recv arena
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ the domain
+struct rpl_domain {
+  rpl_config cfg;
+  Geom g;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void* arena = nullptr;
+  bool own_arena = false;
+  std::vector<int> local;              // global partition indices on this rank
+  void* buf[2][kMaxParts] = {{nullptr}};
+  void** d_tab = nullptr;              // device [2][kMaxParts]
+  int cur = 0;                         // buffer holding the current state
+  bool ghosts_stale = true;
+  unsigned* d_flag = nullptr;
+  unsigned long long* d_smax = nullptr;
+  unsigned* h_flag = nullptr;          // pinned
+  unsigned long long* h_smax = nullptr;
+  void* stage = nullptr;               // AoS set/get staging (lazy)
+  size_t stage_bytes = 0;
+  // multi-rank
+  ncclComm_t comm = nullptr;
+  std::vector<Peer> send_peers, recv_peers;
+  void* d_send = nullptr;
+  void* d_recv = nullptr;
+  int rows = 0;
+  // kernel timing (rpl_profile)
+  std::vector<cudaEvent_t> ev;  // pairs
+  size_t ev_used = 0;
+};
+
+static int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+extern "C" void rpl_config_init(rpl_config* c) {
+  memset(c, 0, sizeof(*c));
+  c->ndim = 1;
+  c->size[0] = c->size[1] = c->size[2] = 1;
+  c->pad = 2;
+  c->parts[0] = c->parts[1] = c->parts[2] = 1;
+  c->dtype = RPL_F64;
+  c->layout = RPL_SOA;
+  c->kernel = RPL_KERNEL_FUSED;
+  c->gamma = 1.4;
+  c->dx[0] = c->dx[1] = c->dx[2] = 1.0;
+  c->nranks = 1;
+}
+
+static rpl_status geom_of(const rpl_config* c, Geom* g) {
+  if (!c) return fail(RPL_E_INVALID_ARG, "null config");
+  const int bl[3] = {c->bc_lo[0], c->bc_lo[1], c->bc_lo[2]};
+  const int bh[3] = {c->bc_hi[0], c->bc_hi[1], c->bc_hi[2]};
+  const int pa[3] = {c->parts[0], c->parts[1], c->parts[2]};
+  const char* why = "";
+  int st = make_geom(c->ndim, c->size, c->pad, pa, c->dtype == RPL_F64 ? 8 : 4, (int)c->layout,
+                     bl, bh, g, &why);
+  if (st) return fail((rpl_status)st, "%s", why);
+  if (!(c->gamma > 1.0)) return fail(RPL_E_INVALID_ARG, "gamma must be > 1");
+  for (int d = 0; d < c->ndim; ++d)
+    if (!(c->dx[d] > 0.0)) return fail(RPL_E_INVALID_ARG, "dx must be > 0");
+  if (c->dtype != RPL_F32 && c->dtype != RPL_F64) return fail(RPL_E_INVALID_ARG, "dtype");
+  if (c->kernel != RPL_KERNEL_FUSED && c->kernel != RPL_KERNEL_SPLIT)
+    return fail(RPL_E_INVALID_ARG, "kernel");
+  if (c->nranks < 1) return fail(RPL_E_INVALID_ARG, "nranks must be >= 1");
+  if (c->nranks > 1 && c->nranks != g->nparts)
+    return fail(RPL_E_INVALID_ARG, "nranks must be 1 or prod(parts) (one partition per rank)");
+  if (c->rank < 0 || c->rank >= c->nranks) return fail(RPL_E_INVALID_ARG, "rank out of range");
+  if (c->nranks > 1 && !c->nccl_id) return fail(RPL_E_INVALID_ARG, "nccl_id required");
+  if (c->rows_per_chunk < 0) return fail(RPL_E_INVALID_ARG, "rows_per_chunk must be >= 0");
+  return RPL_OK;
+}
+
+extern "C" rpl_status rpl_config_check(const rpl_config* c) {
+  Geom g;
+  return geom_of(c, &g);
+}
+
+static int64_t part_bytes(const Geom& g) { return round_up(g.buf_elems * g.elem, 256); }
+
+extern "C" rpl_status rpl_arena_bytes(const rpl_config* c, size_t* out) {
+  Geom g;
+  rpl_status st = geom_of(c, &g);
+  if (st) return st;
+  const int nloc = c->nranks > 1 ? 1 : g.nparts;
+  *out = (size_t)(2 * nloc * part_bytes(g) + 256);
+  return RPL_OK;
+}
+
+extern "C" rpl_status rpl_halo_plan(const rpl_config* c, rpl_halo_edge* edges, int32_t max_edges,
+                                    int32_t* n_edges) {
+  Geom g;
+  rpl_status st = geom_of(c, &g);
+  if (st) return st;
+  std::vector<rpl_halo_edge> v;
+  build_plan(g, &v);
+  if (n_edges) *n_edges = (int32_t)v.size();
+  if (max_edges > 0) {
+    if (!edges) return fail(RPL_E_INVALID_ARG, "null edges");
+    const int n = (int)v.size() < max_edges ? (int)v.size() : max_edges;
+    memcpy(edges, v.data(), sizeof(rpl_halo_edge) * n);
+  }
+  return RPL_OK;
+}
+
+extern "C" rpl_status rpl_nccl_unique_id(void* out128) {
+  if (!out128) return fail(RPL_E_INVALID_ARG, "null out");
+  if (!g_nccl.load()) return fail(RPL_E_NCCL, "libnccl.so.2 not found (set RPL_NCCL_LIB)");
+  ncclUniqueId id;
+  NC(g_nccl.GetUniqueId(&id));
+  memcpy(out128, &id, sizeof(id));
+  return RPL_OK;
+}
+
+static void free_events(rpl_domain* d) {
+  for (auto e : d->ev) cudaEventDestroy(e);
+  d->ev.clear();
+  d->ev_used = 0;
+}
+
+static void free_domain(rpl_domain* d) {
+  if (!d) return;
+  free_events(d);
+  if (d->comm) g_nccl.CommDestroy(d->comm);
+  if (d->own_arena && d->arena) cudaFree(d->arena);
+  if (d->d_tab) cudaFree(d->d_tab);
+  if (d->d_flag) cudaFree(d->d_flag);
+  if (d->d_smax) cudaFree(d->d_smax);
+  if (d->h_flag) cudaFreeHost(d->h_flag);
+  if (d->h_smax) cudaFreeHost(d->h_smax);
+  if (d->stage) cudaFree(d->stage);
+  if (d->d_send) cudaFree(d->d_send);
+  if (d->d_recv) cudaFree(d->d_recv);
+  if (d->own_stream && d->stream) cudaStreamDestroy(d->stream);
+  delete d;
+}
+
+static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
+  d->cfg = *c;
+  rpl_status st = geom_of(c, &d->g);
+  if (st) return st;
+  const Geom& g = d->g;
+  d->device = c->device;
+  CU(cudaSetDevice(d->device));
+  if (c->stream) {
+    d->stream = (cudaStream_t)c->stream;
+  } else {
+    CU(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+    d->own_stream = true;
+  }
+  if (c->nranks > 1) d->local.push_back(c->rank);
+  else
+    for (int p = 0; p < g.nparts; ++p) d->local.push_back(p);
+  size_t bytes = 0;
+  st = rpl_arena_bytes(c, &bytes);
+  if (st) return st;
+  if (c->arena) {
+    d->arena = c->arena;
+  } else {
+    cudaError_t e = cudaMalloc(&d->arena, bytes);
+    if (e != cudaSuccess) return fail(RPL_E_OOM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+    d->own_arena = true;
+  }
+  char* base = (char*)round_up((int64_t)(uintptr_t)d->arena, 256);
+  const int64_t pb = part_bytes(g);
+  for (size_t i = 0; i < d->local.size(); ++i)
+    for (int b = 0; b < 2; ++b) d->buf[b][d->local[i]] = base + (2 * i + b) * pb;
+  CU(cudaMemsetAsync(base, 0, 2 * d->local.size() * pb, d->stream));
+  CU(cudaMalloc(&d->d_tab, sizeof(void*) * 2 * kMaxParts));
+  CU(cudaMemcpy(d->d_tab, d->buf, sizeof(void*) * 2 * kMaxParts, cudaMemcpyHostToDevice));
+  CU(cudaMalloc(&d->d_flag, sizeof(unsigned)));
+  CU(cudaMalloc(&d->d_smax, sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(d->d_flag, 0, sizeof(unsigned), d->stream));
+  CU(cudaMallocHost(&d->h_flag, sizeof(unsigned)));
+  CU(cudaMallocHost(&d->h_smax, sizeof(unsigned long long)));
+  d->rows = c->rows_per_chunk;
+  if (d->rows <= 0) d->rows = g.D == 2 ? auto_rows_2d(g) : (g.D == 3 ? auto_rows_3d(g) : 1);
+  if (c->nranks > 1) {
+    if (!g_nccl.load()) return fail(RPL_E_NCCL, "libnccl.so.2 not found (set RPL_NCCL_LIB)");
+    ncclUniqueId id;
+    memcpy(&id, c->nccl_id, sizeof(id));
+    NC(g_nccl.CommInitRank(&d->comm, c->nranks, id, c->rank));
+    std::vector<rpl_halo_edge> plan;
+    build_plan(g, &plan);
+    const int me = c->rank;
+    auto add = [&](std::vector<Peer>& peers, int peer, const rpl_halo_edge& e) {
+      Peer* P = nullptr;
+      for (auto& q : peers)
+        if (q.rank == peer) P = &q;
+      if (!P) {
+        peers.push_back(Peer());
+        P = &peers.back();
+        P->rank = peer;
+      }
+      DevEdge de;
+      memset(&de, 0, sizeof(de));
+      for (int k = 0; k < 3; ++k) {
+        de.src_lo[k] = e.src_lo[k];
+        de.src_hi[k] = e.src_hi[k];
+        de.dst_lo[k] = e.dst_lo[k];
+        de.dst_hi[k] = e.dst_hi[k];
+        de.mode[k] = e.mode[k];
+      }
+      de.src_part = e.src_part;
+      de.dst_part = e.dst_part;
+      de.count = (e.dst_hi[0] - e.dst_lo[0]) * (e.dst_hi[1] - e.dst_lo[1]) *
+                 (e.dst_hi[2] - e.dst_lo[2]);
+      de.offset = P->elems;
+      P->elems += de.count * g.C;
+      P->edges.push_back(de);
+    };
+    for (const auto& e : plan) {
+      if (e.src_part == me && e.dst_part != me) add(d->send_peers, e.dst_part, e);
+      if (e.dst_part == me && e.src_part != me) add(d->recv_peers, e.src_part, e);
+    }
+    int64_t ns = 0, nr = 0;
+    for (auto& P : d->send_peers) { P.offset = ns; ns += P.elems; }
+    for (auto& P : d->recv_peers) { P.offset = nr; nr += P.elems; }
+    if (ns) CU(cudaMalloc(&d->d_send, ns * g.elem));
+    if (nr) CU(cudaMalloc(&d->d_recv, nr * g.elem));
+  }
+  CU(cudaStreamSynchronize(d->stream));
+  return RPL_OK;
+}
+
+extern "C" rpl_status rpl_create(const rpl_config* c, rpl_domain** out) {
+  if (!out) return fail(RPL_E_INVALID_ARG, "null out");
+  *out = nullptr;
+  rpl_domain* d = new rpl_domain();
+  rpl_status st = create_impl(c, d);
+  if (st != RPL_OK) {
+    std::string keep = g_err;
+    free_domain(d);
+    g_err = keep;
+    return st;
+  }
+  *out = d;
+  return RPL_OK;
+}
+
+extern "C" void rpl_destroy(rpl_domain* d) {
+  if (!d) return;
+  cudaSetDevice(d->device);
+  cudaStreamSynchronize(d->stream);
+  free_domain(d);
+}
+
+extern "C" rpl_status rpl_local_box(const rpl_domain* d, int64_t lo[3], int64_t hi[3]) {
+  if (!d || !lo || !hi) return fail(RPL_E_INVALID_ARG, "null argument");
+  const Geom& g = d->g;
+  if (d->cfg.nranks > 1) {
+    int pc[3];
+    g.part_coords(d->cfg.rank, pc);
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = pc[k] * g.S[k];
+      hi[k] = lo[k] + g.S[k];
+    }
+  } else {
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = 0;
+      hi[k] = g.N[k];
+    }
+  }
+  return RPL_OK;
+}
+
+// host box <-> partition interior copies (dense SoA host [C][bz][by][bx])
+static rpl_status xfer(rpl_domain* d, void* host, bool to_dev) {
+  const Geom& g = d->g;
+  int64_t lo[3], hi[3];
+  rpl_local_box(d, lo, hi);
+  const int64_t bx = hi[0] - lo[0], by = hi[1] - lo[1], bz = hi[2] - lo[2];
+  const size_t el = g.elem;
+  for (int p : d->local) {
+    int pc[3];
+    g.part_coords(p, pc);
+    const int64_t o[3] = {pc[0] * g.S[0] - lo[0], pc[1] * g.S[1] - lo[1], pc[2] * g.S[2] - lo[2]};
+    char* dev = (char*)d->buf[d->cur][p];
+    if (g.layout == 0) {
+      for (int c = 0; c < g.C; ++c) {
+        cudaMemcpy3DParms m;
+        memset(&m, 0, sizeof(m));
+        cudaPitchedPtr hp = make_cudaPitchedPtr((char*)host + (size_t)c * bx * by * bz * el,
+                                                bx * el, bx * el, by);
+        cudaPitchedPtr dp = make_cudaPitchedPtr(dev + (size_t)c * g.comp_stride * el, g.pitch * el,
+                                                g.pitch * el, g.P[1]);
+        const cudaPos hpos = make_cudaPos(o[0] * el, o[1], o[2]);
+        const cudaPos dpos = make_cudaPos(g.xo * el, g.off[1], g.off[2]);
+        if (to_dev) {
+          m.srcPtr = hp; m.srcPos = hpos; m.dstPtr = dp; m.dstPos = dpos;
+          m.kind = cudaMemcpyHostToDevice;
+        } else {
+          m.srcPtr = dp; m.srcPos = dpos; m.dstPtr = hp; m.dstPos = hpos;
+          m.kind = cudaMemcpyDeviceToHost;
+        }
+        m.extent = make_cudaExtent(g.S[0] * el, g.S[1], g.S[2]);
+        CU(cudaMemcpy3DAsync(&m, d->stream));
+      }
+    } else {
+      const size_t need = (size_t)g.C * g.cells() * el;
+      if (d->stage_bytes < need) {
+        CU(cudaStreamSynchronize(d->stream));
+        if (d->stage) cudaFree(d->stage);
+        d->stage = nullptr;
+        d->stage_bytes = 0;
+        CU(cudaMalloc(&d->stage, need));
+        d->stage_bytes = need;
+      }
+      for (int c = 0; c < g.C; ++c) {
+        cudaMemcpy3DParms m;
+        memset(&m, 0, sizeof(m));
+        cudaPitchedPtr hp = make_cudaPitchedPtr((char*)host + (size_t)c * bx * by * bz * el,
+                                                bx * el, bx * el, by);
+        cudaPitchedPtr sp = make_cudaPitchedPtr((char*)d->stage + (size_t)c * g.cells() * el,
+                                                g.S[0] * el, g.S[0] * el, g.S[1]);
+        const cudaPos hpos = make_cudaPos(o[0] * el, o[1], o[2]);
+        if (to_dev) {
+          m.srcPtr = hp; m.srcPos = hpos; m.dstPtr = sp; m.kind = cudaMemcpyHostToDevice;
+        } else {
+          m.srcPtr = sp; m.dstPtr = hp; m.dstPos = hpos; m.kind = cudaMemcpyDeviceToHost;
+        }
+        m.extent = make_cudaExtent(g.S[0] * el, g.S[1], g.S[2]);
+        if (to_dev) {
+          CU(cudaMemcpy3DAsync(&m, d->stream));
+        }
+        if (!to_dev && c == 0) {
+          if (el == 8) launch_stage<double>(g, (double*)dev, (double*)d->stage, 1, d->stream);
+          else launch_stage<float>(g, (float*)dev, (float*)d->stage, 1, d->stream);
+          CU(cudaGetLastError());
+        }
+        if (!to_dev) CU(cudaMemcpy3DAsync(&m, d->stream));
+      }
+      if (to_dev) {
+        if (el == 8) launch_stage<double>(g, (double*)dev, (double*)d->stage, 0, d->stream);
+        else launch_stage<float>(g, (float*)dev, (float*)d->stage, 0, d->stream);
+        CU(cudaGetLastError());
+      }
+    }
+  }
+  return RPL_OK;
+}
+
+static rpl_status check_flag(rpl_domain* d) {
+  CU(cudaMemcpyAsync(d->h_flag, d->d_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, d->stream));
+  CU(cudaStreamSynchronize(d->stream));
+  if (*d->h_flag)
+    return fail(RPL_E_DOMAIN, "numerical-domain error: rho<=0, p<=0 or non-finite state (S:588)");
+  return RPL_OK;
+}
+
+extern "C" rpl_status rpl_set_state(rpl_domain* d, const void* host) {
+  if (!d || !host) return fail(RPL_E_INVALID_ARG, "null argument");
+  CU(cudaSetDevice(d->device));
+  rpl_status st = xfer(d, (void*)host, true);
+  if (st) return st;
+  CU(cudaMemsetAsync(d->d_flag, 0, sizeof(unsigned), d->stream));
+  CU(cudaStreamSynchronize(d->stream));
+  d->ghosts_stale = true;
+  return RPL_OK;
+}
+
+extern "C" rpl_status rpl_get_state(rpl_domain* d, void* host) {
+  if (!d || !host) return fail(RPL_E_INVALID_ARG, "null argument");
+  CU(cudaSetDevice(d->device));
+  rpl_status st = xfer(d, host, false);
+  if (st) return st;
+  CU(cudaStreamSynchronize(d->stream));
+  return check_flag(d);
+}
+
+extern "C" rpl_status rpl_get_padded(rpl_domain* d, int32_t part, void* host) {
+  if (!d || !host) return fail(RPL_E_INVALID_ARG, "null argument");
+  const Geom& g = d->g;
+  if (part < 0 || part >= g.nparts || !d->buf[d->cur][part])
+    return fail(RPL_E_INVALID_ARG, "partition %d is not on this rank", part);
+  CU(cudaSetDevice(d->device));
+  std::vector<char> raw((size_t)g.buf_elems * g.elem);
+  CU(cudaMemcpyAsync(raw.data(), d->buf[d->cur][part], raw.size(), cudaMemcpyDeviceToHost,
+                     d->stream));
+  CU(cudaStreamSynchronize(d->stream));
+  const int64_t n = g.P[0] * g.P[1] * g.P[2];
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t x = i % g.P[0] - g.off[0], y = (i / g.P[0]) % g.P[1] - g.off[1],
+                  z = i / (g.P[0] * g.P[1]) - g.off[2];
+    for (int c = 0; c < g.C; ++c)
+      memcpy((char*)host + ((size_t)c * n + i) * g.elem,
+             raw.data() + (size_t)g.at(c, x, y, z) * g.elem, g.elem);
+  }
+  return RPL_OK;
+}
+
+template <typename T>
+static rpl_status exchange_t(rpl_domain* d, int b) {
+  const Geom& g = d->g;
+  T* mine = (T*)d->buf[b][d->cfg.rank];
+  for (auto& P : d->send_peers)
+    for (auto& e : P.edges) launch_edge<T>(g, e, mine, (T*)d->d_send + P.offset + e.offset, 0, d->stream);
+  CU(cudaGetLastError());
+  const ncclDataType_t ty = g.elem == 8 ? ncclFloat64 : ncclFloat32;
+  NC(g_nccl.GroupStart());
+  for (auto& P : d->send_peers)
+    NC(g_nccl.Send((T*)d->d_send + P.offset, P.elems, ty, P.rank, d->comm, d->stream));
+  for (auto& P : d->recv_peers)
+    NC(g_nccl.Recv((T*)d->d_recv + P.offset, P.elems, ty, P.rank, d->comm, d->stream));
+  NC(g_nccl.GroupEnd());
+  for (auto& P : d->recv_peers)
+    for (auto& e : P.edges) launch_edge<T>(g, e, mine, (T*)d->d_recv + P.offset + e.offset, 1, d->stream);
+  CU(cudaGetLastError());
+  return RPL_OK;
+}
+
+static rpl_status exchange(rpl_domain* d, int b) {
+  if (d->cfg.nranks <= 1) return RPL_OK;
+  return d->g.elem == 8 ? exchange_t<double>(d, b) : exchange_t<float>(d, b);
+}
+
+template <typename T>
+static rpl_status fill_t(rpl_domain* d) {
+  T* const* tab = (T* const*)(d->d_tab + d->cur * kMaxParts);
+  for (int p : d->local) launch_fill<T>(d->g, p, tab, d->stream);
+  CU(cudaGetLastError());
+  return exchange(d, d->cur);
+}
+
+extern "C" rpl_status rpl_fill_padding(rpl_domain* d) {
+  if (!d) return fail(RPL_E_INVALID_ARG, "null domain");
+  CU(cudaSetDevice(d->device));
+  rpl_status st = d->g.elem == 8 ? fill_t<double>(d) : fill_t<float>(d);
+  if (st) return st;
+  d->ghosts_stale = false;
+  return RPL_OK;
+}
+
+static bool use_fused(const rpl_domain* d) {
+  return d->cfg.kernel == RPL_KERNEL_FUSED && d->g.layout == 0 && d->g.D == 2;
+}
+
+extern "C" rpl_status rpl_launches_per_step(const rpl_domain* d, int32_t* out) {
+  if (!d || !out) return fail(RPL_E_INVALID_ARG, "null argument");
+  int n = (int)d->local.size() * (use_fused(d) ? 1 : d->g.D);
+  int ne = 0;
+  for (auto& P : d->send_peers) ne += (int)P.edges.size();
+  for (auto& P : d->recv_peers) ne += (int)P.edges.size();
+  n += ne * (use_fused(d) ? 1 : d->g.D);
+  *out = n;
+  return RPL_OK;
+}
+
+template <typename T>
+static rpl_status advance_t(rpl_domain* d, double dt, int nsteps) {
+  const Geom& g = d->g;
+  KArgs<T> a;
+  memset(&a, 0, sizeof(a));
+  a.g = g;
+  for (int k = 0; k < 3; ++k) {
+    const double lam = k < g.D ? dt / d->cfg.dx[k] : 0.0;
+    a.q[k] = (T)(0.25 * lam);
+    a.nq2[k] = (T)(-0.25 * lam * lam);
+  }
+  a.gm1 = (T)(d->cfg.gamma - 1.0);
+  a.flag = d->d_flag;
+  a.rows = d->rows;
+  const bool fused = use_fused(d);
+  for (int s = 0; s < nsteps; ++s) {
+    const int nsweep = fused ? 1 : g.D;
+    for (int sw = 0; sw < nsweep; ++sw) {
+      const int nb = d->cur ^ 1;
+      a.outs = (T* const*)(d->d_tab + nb * kMaxParts);
+      for (int p : d->local) {
+        a.part = p;
+        g.part_coords(p, a.pc);
+        for (int k = 0; k < 3; ++k) a.lo[k] = a.pc[k] * g.S[k];
+        a.in = (const T*)d->buf[d->cur][p];
+        a.out = (T*)d->buf[nb][p];
+        const bool prof = d->ev_used + 2 <= d->ev.size();
+        if (prof) cudaEventRecord(d->ev[d->ev_used], d->stream);
+        if (fused) launch_step2d<T>(a, d->stream);
+        else launch_sweep<T>(a, sw, d->stream);
+        if (prof) {
+          cudaEventRecord(d->ev[d->ev_used + 1], d->stream);
+          d->ev_used += 2;
+        }
+      }
+      CU(cudaGetLastError());
+      rpl_status st = exchange(d, nb);
+      if (st) return st;
+      d->cur = nb;  // Listing 8 swap: the current state is the last-written buffer
+    }
+  }
+  return RPL_OK;
+}
+
+extern "C" rpl_status rpl_advance(rpl_domain* d, double dt, int32_t nsteps) {
+  if (!d) return fail(RPL_E_INVALID_ARG, "null domain");
+  if (!(dt > 0.0) || nsteps < 0) return fail(RPL_E_INVALID_ARG, "dt must be > 0, nsteps >= 0");
+  CU(cudaSetDevice(d->device));
+  if (d->ghosts_stale) {
+    rpl_status st = rpl_fill_padding(d);
+    if (st) return st;
+  }
+  return d->g.elem == 8 ? advance_t<double>(d, dt, nsteps) : advance_t<float>(d, dt, nsteps);
+}
+
+extern "C" rpl_status rpl_max_wavespeed(rpl_domain* d, double* out) {
+  if (!d || !out) return fail(RPL_E_INVALID_ARG, "null argument");
+  CU(cudaSetDevice(d->device));
+  CU(cudaMemsetAsync(d->d_smax, 0, sizeof(unsigned long long), d->stream));
+  for (int p : d->local) {
+    if (d->g.elem == 8)
+      launch_maxws<double>(d->g, (const double*)d->buf[d->cur][p], d->cfg.gamma, d->d_smax,
+                           d->d_flag, d->stream);
+    else
+      launch_maxws<float>(d->g, (const float*)d->buf[d->cur][p], d->cfg.gamma, d->d_smax,
+                          d->d_flag, d->stream);
+  }
+  CU(cudaGetLastError());
+  if (d->cfg.nranks > 1)
+    NC(g_nccl.AllReduce(d->d_smax, d->d_smax, 1, ncclUint64, ncclMax, d->comm, d->stream));
+  CU(cudaMemcpyAsync(d->h_smax, d->d_smax, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     d->stream));
+  rpl_status st = check_flag(d);
+  if (st) return st;
+  unsigned long long bits = *d->h_smax;
+  memcpy(out, &bits, sizeof(double));
+  return RPL_OK;
+}
+
+extern "C" rpl_status rpl_advance_cfl(rpl_domain* d, double t_end, double cfl, int32_t n_reduced,
+                                      double reduce, int32_t max_steps, int32_t* nsteps_out) {
+  if (!d) return fail(RPL_E_INVALID_ARG, "null domain");
+  if (!(cfl > 0.0) || !(t_end >= 0.0) || max_steps < 0)
+    return fail(RPL_E_INVALID_ARG, "cfl > 0, t_end >= 0, max_steps >= 0 required");
+  double dxmin = d->cfg.dx[0];
+  for (int k = 1; k < d->g.D; ++k)
+    if (d->cfg.dx[k] < dxmin) dxmin = d->cfg.dx[k];
+  double t = 0.0;
+  int n = 0;
+  rpl_status st = RPL_OK;
+  while (t < t_end && n < max_steps) {
+    double S = 0.0;
+    st = rpl_max_wavespeed(d, &S);
+    if (st) break;
+    if (!(S > 0.0)) { st = fail(RPL_E_DOMAIN, "max wavespeed is not positive"); break; }
+    const double c = n < n_reduced ? cfl * reduce : cfl;
+    double dt = c * dxmin / S;
+    bool last = false;
+    if (t + dt >= t_end) {
+      dt = t_end - t;
+      last = true;
+    }
+    st = rpl_advance(d, dt, 1);
+    ++n;
+    if (st) break;
+    t = last ? t_end : t + dt;
+  }
+  if (nsteps_out) *nsteps_out = n;
+  if (st) return st;
+  return rpl_synchronize(d);
+}
+
+extern "C" rpl_status rpl_synchronize(rpl_domain* d) {
+  if (!d) return fail(RPL_E_INVALID_ARG, "null domain");
+  CU(cudaSetDevice(d->device));
+  CU(cudaStreamSynchronize(d->stream));
+  CU(cudaGetLastError());
+  return check_flag(d);
+}
+
+extern "C" rpl_status rpl_profile(rpl_domain* d, int32_t max_launches) {
+  if (!d || max_launches < 0) return fail(RPL_E_INVALID_ARG, "bad argument");
+  CU(cudaSetDevice(d->device));
+  CU(cudaStreamSynchronize(d->stream));
+  free_events(d);
+  for (int i = 0; i < 2 * max_launches; ++i) {
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    d->ev.push_back(e);
+  }
+  return RPL_OK;
+}
+
+extern "C" rpl_status rpl_profile_read(rpl_domain* d, double* kernel_ms, int64_t* launches) {
+  if (!d || !kernel_ms || !launches) return fail(RPL_E_INVALID_ARG, "null argument");
+  CU(cudaSetDevice(d->device));
+  CU(cudaStreamSynchronize(d->stream));
+  double tot = 0.0;
+  for (size_t i = 0; i + 1 < d->ev_used; i += 2) {
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, d->ev[i], d->ev[i + 1]));
+    tot += ms;
+  }
+  *kernel_ms = tot;
+  *launches = (int64_t)(d->ev_used / 2);
+  d->ev_used = 0;
+  return RPL_OK;
+}

@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerance (BASELINE.json north_star): max relative error <= 1e-10 in fp64 and
+<= 1e-4 in fp32 after 100 steps, relative error per component as in DESIGN.md
+reading S15: max_i |g - o| / max_i |o|.  Partitioned runs, split vs fused
+kernels and AoS vs SoA must be bitwise identical.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2104_08571_b200 as R
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+OK = {"clamp": oracle.BC_TRANSMISSIVE, "periodic": oracle.BC_PERIODIC,
+      "reflective": oracle.BC_REFLECTIVE}
+
+
+def relerr(g, o):
+    """DESIGN.md reading S15: max over components of max|g-o| / max|o|, where the
+    momentum components share one scale (max over all momentum components), so a
+    transverse momentum that is ~0 everywhere is not divided by itself."""
+    C = o.shape[-1]
+    o64, g64 = o.astype(np.float64), g.astype(np.float64)
+    mom = np.max(np.abs(o64[..., 1:C - 1])) if C > 2 else 0.0
+    errs = []
+    for c in range(C):
+        scale = np.max(np.abs(o64[..., c]))
+        if 0 < c < C - 1:
+            scale = max(scale, mom)
+        diff = np.max(np.abs(g64[..., c] - o64[..., c]))
+        errs.append(diff / scale if scale > 0 else diff)
+    return max(errs)
+
+
+def run_gpu(U0, dt, nsteps, dtype="f64", **kw):
+    n = tuple(reversed(U0.shape[:-1]))
+    with R.Domain(n, dtype=dtype, **kw) as dom:
+        dom.set_state(U0)
+        dom.advance(dt, nsteps)
+        return dom.get_state()
+
+
+def run_oracle(U0, dt, nsteps, dx, pad=2, bc_lo=None, bc_hi=None):
+    n = tuple(reversed(U0.shape[:-1]))
+    D = len(n)
+    g = oracle.Grid(n, pad=pad, dx=dx, bc_lo=[OK[b] for b in (bc_lo or ["clamp"] * D)],
+                    bc_hi=[OK[b] for b in (bc_hi or ["clamp"] * D)])
+    return oracle.step(g, U0, dt, nsteps)
+
+
+def test_sod_cfl_run_matches_oracle():
+    N = 200
+    U0 = W.sod(N)
+    with R.Domain((N,), pad=2) as dom:
+        dom.set_state(U0)
+        n = dom.advance_cfl(0.2, cfl=0.9, n_reduced=5, reduce=0.2)
+        Ug = dom.get_state()
+    Uo, no = oracle.run_cfl(oracle.Grid((N,), pad=2), U0, 0.2)
+    assert n == no == 100
+    assert relerr(Ug, Uo) <= 1e-10
+
+
+@pytest.mark.parametrize("kernel", ["fused", "split"])
+@pytest.mark.parametrize("workload", ["random", "shock_bubble"])
+def test_2d_100_steps_fp64(kernel, workload):
+    n = (192, 160)
+    dx = [1.0 / 192] * 2
+    U0 = W.random_state(n) if workload == "random" else W.shock_bubble(n, dx=dx)
+    dt = 0.4 * dx[0] / oracle.max_wavespeed(oracle.Grid(n), U0)
+    Ug = run_gpu(U0, dt, 100, kernel=kernel, dx=dx)
+    Uo = run_oracle(U0, dt, 100, dx)
+    assert relerr(Ug, Uo) <= 1e-10
+
+
+@pytest.mark.parametrize("bc", ["periodic", "reflective"])
+def test_2d_boundary_kinds(bc):
+    n = (130, 70)   # ragged: 130 = 2 windows of 62 + 6
+    dx = [1.0 / 130] * 2
+    U0 = W.random_state(n, seed=3)
+    dt = 0.4 * dx[0] / oracle.max_wavespeed(oracle.Grid(n), U0)
+    Ug = run_gpu(U0, dt, 60, dx=dx, bc_lo=[bc, bc], bc_hi=[bc, bc])
+    Uo = run_oracle(U0, dt, 60, dx, bc_lo=[bc, bc], bc_hi=[bc, bc])
+    assert relerr(Ug, Uo) <= 1e-10
+
+
+def test_3d_fp64():
+    n = (28, 24, 20)
+    dx = [1.0 / 28] * 3
+    U0 = W.shock_bubble(n, dx=dx)
+    dt = 0.4 * dx[0] / oracle.max_wavespeed(oracle.Grid(n), U0)
+    Ug = run_gpu(U0, dt, 100, dx=dx)
+    Uo = run_oracle(U0, dt, 100, dx)
+    assert relerr(Ug, Uo) <= 1e-10
+
+
+def test_3d_mixed_bcs():
+    n = (16, 12, 10)
+    dx = [1.0 / 16] * 3
+    bl = ["reflective", "periodic", "clamp"]
+    bh = ["clamp", "periodic", "reflective"]
+    U0 = W.random_state(n, seed=5)
+    dt = 0.4 * dx[0] / oracle.max_wavespeed(oracle.Grid(n), U0)
+    Ug = run_gpu(U0, dt, 50, dx=dx, bc_lo=bl, bc_hi=bh)
+    Uo = run_oracle(U0, dt, 50, dx, bc_lo=bl, bc_hi=bh)
+    assert relerr(Ug, Uo) <= 1e-10
+
+
+@pytest.mark.parametrize("n", [(128, 96), (24, 20, 16)])
+def test_fp32_against_fp32_oracle(n):
+    D = len(n)
+    dx = [1.0 / n[0]] * D
+    U0 = W.shock_bubble(n, dx=dx).astype(np.float32)
+    dt = 0.4 * dx[0] / oracle.max_wavespeed(oracle.Grid(n), U0.astype(np.float64))
+    Ug = run_gpu(U0, dt, 100, dtype="f32", dx=dx)
+    Uo = run_oracle(U0, dt, 100, dx)
+    assert Uo.dtype == np.float32
+    assert relerr(Ug, Uo) <= 1e-4
+
+
+@pytest.mark.parametrize("n,parts", [((128, 96), (2, 2)), ((128, 96), (1, 4)),
+                                     ((128, 96), (4, 1)), ((24, 16, 16), (2, 2, 2)),
+                                     ((24, 16, 16), (1, 1, 4)), ((200,), (4,))])
+@pytest.mark.parametrize("bc", ["clamp", "periodic", "reflective"])
+def test_partitioned_bitwise_identical(n, parts, bc):
+    D = len(n)
+    dx = [1.0 / n[0]] * D
+    U0 = W.random_state(n, seed=9)
+    dt = 0.3 * dx[0] / 3.0
+    kw = dict(dx=dx, bc_lo=[bc] * D, bc_hi=[bc] * D)
+    one = run_gpu(U0, dt, 20, **kw)
+    many = run_gpu(U0, dt, 20, parts=parts, **kw)
+    assert np.array_equal(one, many)
+
+
+def test_split_fused_and_layouts_bitwise():
+    n = (140, 66)
+    dx = [1.0 / 140] * 2
+    U0 = W.shock_bubble(n, dx=dx)
+    dt = 0.4 * dx[0] / 5.8
+    a = run_gpu(U0, dt, 30, dx=dx, kernel="fused")
+    b = run_gpu(U0, dt, 30, dx=dx, kernel="split")
+    c = run_gpu(U0, dt, 30, dx=dx, kernel="split", layout="aos")
+    d = run_gpu(U0, dt, 30, dx=dx, kernel="fused", rows_per_chunk=5)
+    assert np.array_equal(a, b) and np.array_equal(a, c) and np.array_equal(a, d)
+
+
+@pytest.mark.parametrize("n,parts", [((20, 12), (2, 3)), ((10, 8, 6), (2, 2, 3))])
+def test_fill_padding_halo_soundness(n, parts):
+    """After fill_padding every ghost equals the single-block value."""
+    D = len(n)
+    bl = ["reflective", "periodic", "clamp"][:D]
+    bh = ["clamp", "periodic", "reflective"][:D]
+    U0 = W.random_state(n, seed=21)
+    g = oracle.Grid(n, pad=2, bc_lo=[OK[b] for b in bl], bc_hi=[OK[b] for b in bh])
+    P = np.zeros(oracle.padded_shape(g))
+    P[tuple(slice(2, 2 + n[d]) for d in reversed(range(D)))] = U0
+    P = oracle.fill_ghosts(g, P)
+    S = [n[d] // parts[d] for d in range(D)]
+    with R.Domain(n, parts=parts, bc_lo=bl, bc_hi=bh) as dom:
+        dom.set_state(U0)
+        dom.fill_padding()
+        for p in range(int(np.prod(parts))):
+            pc = np.unravel_index(p, tuple(reversed(parts)))[::-1]
+            got = np.moveaxis(dom.get_padded(p), 0, -1)
+            sl = tuple(slice(pc[d] * S[d], pc[d] * S[d] + S[d] + 4) for d in reversed(range(D)))
+            assert np.array_equal(got, P[sl]), p
+
+
+def test_ghosts_after_advance_are_sound():
+    """The fused kernel's ghost images equal a fresh fill of the same state."""
+    n = (130, 40)
+    U0 = W.random_state(n, seed=2)
+    kw = dict(bc_lo=["reflective", "periodic"], bc_hi=["clamp", "periodic"], parts=(2, 2))
+    with R.Domain(n, **kw) as dom:
+        dom.set_state(U0)
+        dom.advance(1e-4, 3)
+        after = [dom.get_padded(p) for p in range(4)]
+        dom.set_state(dom.get_state())
+        dom.fill_padding()
+        fresh = [dom.get_padded(p) for p in range(4)]
+    for a, b in zip(after, fresh):
+        assert np.array_equal(a, b)
+
+
+def test_max_wavespeed_matches_oracle():
+    for n in [(1000,), (96, 80), (20, 18, 16)]:
+        U0 = W.shock_bubble(n, dx=[1.0 / n[0]] * len(n)) if len(n) > 1 else W.sod(n[0])
+        with R.Domain(n, parts=(2,) + (1,) * (len(n) - 1)) as dom:
+            dom.set_state(U0)
+            s = dom.max_wavespeed()
+        so = oracle.max_wavespeed(oracle.Grid(n), U0)
+        assert abs(s - so) <= 1e-14 * so
+
+
+def test_domain_error_is_reported():
+    n = (64, 64)
+    U0 = W.uniform(n)
+    U0[..., 3] = -1.0
+    with R.Domain(n) as dom:
+        dom.set_state(U0)
+        dom.advance(1e-3, 1)
+        with pytest.raises(R.DomainError):
+            dom.synchronize()
+
+
+def test_uniform_state_bitwise_full_size():
+    """BASELINE configs[1] size and launch configuration: uniform state is a fixed point."""
+    n = (1024, 1024)
+    U0 = W.uniform(n, rho=0.9, vel=[0.4, -0.3], p=1.2)
+    Ug = run_gpu(U0, 1e-4, 5)
+    assert np.array_equal(Ug, U0)
+
+
+def _patch_oracle(Uin, lo, hi, n, k, dt, dx, bcs):
+    """Oracle on a sub-box [lo,hi) of the full input; valid region shrinks by k per cut side."""
+    D = len(n)
+    sl = tuple(slice(lo[d], hi[d]) for d in reversed(range(D)))
+    sub = np.ascontiguousarray(Uin[sl])
+    pn = tuple(hi[d] - lo[d] for d in range(D))
+    g = oracle.Grid(pn, pad=2, dx=dx, bc_lo=[OK[bcs] if lo[d] == 0 else oracle.BC_TRANSMISSIVE
+                                             for d in range(D)],
+                    bc_hi=[OK[bcs] if hi[d] == n[d] else oracle.BC_TRANSMISSIVE for d in range(D)])
+    out = oracle.step(g, sub, dt, k)
+    v0 = [0 if lo[d] == 0 else k for d in range(D)]
+    v1 = [pn[d] if hi[d] == n[d] else pn[d] - k for d in range(D)]
+    vsl = tuple(slice(v0[d], v1[d]) for d in reversed(range(D)))
+    gsl = tuple(slice(lo[d] + v0[d], lo[d] + v1[d]) for d in reversed(range(D)))
+    return out[vsl], gsl
+
+
+def test_full_size_sampled_parity_2d1024():
+    """configs[1] (1024^2 fp64, bench launch config): sampled patches vs the oracle."""
+    n = (1024, 1024)
+    dx = [1.0 / 1024] * 2
+    U0 = W.shock_bubble(n, dx=dx)
+    dt = 0.4 * dx[0] / oracle.max_wavespeed(oracle.Grid(n), U0)
+    k = 4
+    Ug = run_gpu(U0, dt, k, dx=dx)
+    for lo in [(0, 0), (980, 0), (90, 500), (400, 440), (1000, 1000), (0, 990), (600, 100)]:
+        hi = (min(lo[0] + 44, 1024), min(lo[1] + 44, 1024))
+        ref, gsl = _patch_oracle(U0, lo, hi, n, k, dt, dx, "clamp")
+        assert relerr(Ug[gsl], ref) <= 1e-12, lo

@@ -38,17 +38,34 @@ def uniform_pm1(seed: int, stream: int, index: np.ndarray) -> np.ndarray:
     return (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -52) - 1.0
 
 
-def _global_index(n):
-    """Global linear cell index (x fastest) with shape (nz, ny, nx) trimmed to ndim."""
-    size = int(np.prod(n))
-    return np.arange(size, dtype=np.uint64).reshape(tuple(reversed(n)))
+def _box(n, box):
+    D = len(n)
+    if box is None:
+        return [0] * D, list(n)
+    lo, hi = box
+    return [int(v) for v in lo[:D]], [int(v) for v in hi[:D]]
 
 
-def _coords(n, dx, origin=None):
-    """Cell-centre coordinates x_d = (i_d + 1/2) dx_d, each with the grid's shape."""
+def _global_index(n, box=None):
+    """Global linear cell index (x fastest) of the cells of `box` (default: the whole
+    grid), shape (nz, ny, nx) trimmed to ndim."""
+    D = len(n)
+    lo, hi = _box(n, box)
+    axes = [np.arange(lo[d], hi[d], dtype=np.uint64) for d in range(D)]
+    stride = [int(np.prod(n[:d])) for d in range(D)]
+    mesh = np.meshgrid(*reversed(axes), indexing="ij")
+    idx = np.zeros(mesh[0].shape, dtype=np.uint64)
+    for d in range(D):
+        idx += mesh[D - 1 - d] * np.uint64(stride[d])
+    return idx
+
+
+def _coords(n, dx, origin=None, box=None):
+    """Cell-centre coordinates x_d = (i_d + 1/2) dx_d of the cells of `box`."""
     D = len(n)
     origin = origin or [0.0] * D
-    axes = [origin[d] + (np.arange(n[d]) + 0.5) * dx[d] for d in range(D)]
+    lo, hi = _box(n, box)
+    axes = [origin[d] + (np.arange(lo[d], hi[d]) + 0.5) * dx[d] for d in range(D)]
     mesh = np.meshgrid(*reversed(axes), indexing="ij")  # (z, y, x) order
     return list(reversed(mesh))  # [x, y, z]
 
@@ -70,10 +87,11 @@ def uniform(n, rho=1.0, vel=None, p=1.0, gamma=GAMMA):
                      gamma)
 
 
-def random_state(n, seed=SEED, gamma=GAMMA, rho=(0.5, 1.5), vel=0.5, p=(0.5, 1.5)):
-    """Random positive state: rho, p uniform in the given ranges, |u_k| <= vel."""
+def random_state(n, seed=SEED, gamma=GAMMA, rho=(0.5, 1.5), vel=0.5, p=(0.5, 1.5), box=None):
+    """Random positive state: rho, p uniform in the given ranges, |u_k| <= vel.
+    `box` = (lo, hi) restricts generation to a sub-box of the global grid."""
     D = len(n)
-    idx = _global_index(n)
+    idx = _global_index(n, box)
     r = rho[0] + (rho[1] - rho[0]) * 0.5 * (uniform_pm1(seed, 0, idx) + 1.0)
     vs = [vel * uniform_pm1(seed, 1 + k, idx) for k in range(D)]
     pr = p[0] + (p[1] - p[0]) * 0.5 * (uniform_pm1(seed, 4, idx) + 1.0)
@@ -133,14 +151,14 @@ def mach_shock_state(mach=3.81, pre=(1.0, 0.0, 1.0), gamma=GAMMA):
 
 
 def shock_bubble(n, dx=None, seed=SEED, gamma=GAMMA, shock_x=0.1, radius=0.15,
-                 bubble_rho=0.1, perturb=1e-3, origin=None):
+                 bubble_rho=0.1, perturb=1e-3, origin=None, box=None):
     """Mach 3.81 shock hitting a light bubble (the paper's scaling workload, P:1369-1373,
     geometry of SURVEY 8(d)): post-shock state for x < shock_x, quiescent (1,0,1)
     elsewhere, bubble of density bubble_rho centred at (0.4, L_y/2, L_z/2), and
     rho *= (1 + perturb * xi) with xi ~ U[-1,1) from the hash generator."""
     D = len(n)
     dx = dx if dx is not None else [1.0 / n[0]] * D
-    X = _coords(n, dx, origin)
+    X = _coords(n, dx, origin, box)
     L = [n[d] * dx[d] for d in range(D)]
     r2, u2, p2 = mach_shock_state(3.81, (1.0, 0.0, 1.0), gamma)
     post = X[0] < shock_x
@@ -150,7 +168,7 @@ def shock_bubble(n, dx=None, seed=SEED, gamma=GAMMA, shock_x=0.1, radius=0.15,
     rho = np.where(post, r2, np.where(bubble, bubble_rho, 1.0))
     u = np.where(post, u2, 0.0)
     p = np.where(post, p2, 1.0)
-    xi = uniform_pm1(seed, 5, _global_index(n))
+    xi = uniform_pm1(seed, 5, _global_index(n, box))
     rho = rho * (1.0 + perturb * xi)
     vel = [u] + [np.zeros_like(u) for _ in range(1, D)]
     return conserved(rho, vel, p, gamma)
