@@ -236,7 +236,9 @@ def main():
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
-    stream = torch.cuda.current_stream()
+    # a real (non-default) stream shared by the library, the events and the L2 flush
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
 
     gn, parts = decomposition(wl, world)
     D = wl["ndim"]

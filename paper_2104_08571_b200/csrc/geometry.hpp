@@ -6,10 +6,13 @@
 // face (uniform padding S:194).
 //
 // HBM layout of one partition buffer:
-//   SoA ("strided"):  [C][Pz][Py][pitch]    element (c,x,y,z) at
-//       c*comp_stride + ((z+oz)*Py + (y+oy))*pitch + xo + x
-//   AoS ("contiguous"):          [Pz][Py][pitch][C]    cell (x,y,z) at
-//       (((z+oz)*Py + (y+oy))*pitch + xo + x)*C + c
+//   SoA ("strided"):  [Pz][Py][C][pitch]   -- every row holds C
+//       component sub-rows, each contiguous in x (coalesced 128-bit vectors);
+//       component c of row r sits c*pitch elements after component 0
+//   AoS ("contiguous"):          [Pz][Py][pitch][C]
+// element (c,x,y,z) at  row(y,z)*rstride + c*cstride + (xo+x)*xstride  with
+//   SoA: rstride = C*pitch, cstride = pitch, xstride = 1
+//   AoS: rstride = C*pitch, cstride = 1,     xstride = C
 // Pd = S_d + 2 pad for used dims, 1 for unused dims (oz/oy = pad or 0).
 // xo is chosen odd-aligned so that x = -1 starts a 2-element vector (the fused
 // kernel's 64-slot warp windows start at x = 62k - 1) and `pitch` is a multiple
@@ -45,7 +48,9 @@ struct Geom {
   int64_t off[3];     // padded index of interior cell 0 (pad or 0)
   int64_t xo;         // row offset of x = 0 (== off[0] shifted for alignment)
   int64_t pitch;      // elements (SoA) or cells (AoS) per row
-  int64_t comp_stride;  // SoA: elements per component; AoS: unused
+  int64_t rstride;    // elements between consecutive rows (both layouts: C*pitch)
+  int64_t cstride;    // elements between components of one cell (SoA pitch, AoS 1)
+  int64_t xstride;    // elements between consecutive x cells (SoA 1, AoS C)
   int64_t buf_elems;  // elements per partition buffer
   int nwin;           // fused: 62-cell windows per row
 
@@ -53,8 +58,7 @@ struct Geom {
   RPL_HD int64_t row(int64_t y, int64_t z) const { return (z + off[2]) * P[1] + (y + off[1]); }
   // element index of component c of cell (x, y, z)
   RPL_HD int64_t at(int c, int64_t x, int64_t y, int64_t z) const {
-    return layout == 0 ? c * comp_stride + row(y, z) * pitch + xo + x
-                       : (row(y, z) * pitch + xo + x) * C + c;
+    return row(y, z) * rstride + c * cstride + (xo + x) * xstride;
   }
   RPL_HD int64_t cells() const { return S[0] * S[1] * S[2]; }
   RPL_HD void part_coords(int p, int pc[3]) const {

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "async.cuh"
 #include "kernels.hpp"
 #include "scheme.cuh"
 
@@ -33,17 +34,22 @@ template <int D, int L, typename T>
 __device__ __forceinline__ void load_cell(const Geom& g, const T* __restrict__ buf, int64_t x,
                                           int64_t y, int64_t z, T* v) {
 #pragma unroll
-  for (int c = 0; c < D + 2; ++c) {
-    const int64_t i = L == 0 ? c * g.comp_stride + g.row(y, z) * g.pitch + g.xo + x
-                             : (g.row(y, z) * g.pitch + g.xo + x) * (D + 2) + c;
-    v[c] = buf[i];
-  }
+  for (int c = 0; c < D + 2; ++c) v[c] = buf[g.at(c, x, y, z)];
+}
+
+// Cold path: ghost images of one boundary cell.  Values travel in registers,
+// the launch arguments are read in place (__grid_constant__).
+template <int D, int L, typename T>
+__device__ __noinline__ void images_nl(const KArgs<T>* a, int64_t x, int64_t y, int64_t z, T v0,
+                                       T v1, T v2, T v3, T v4) {
+  const T v[5] = {v0, v1, v2, v3, v4};
+  write_images<D, L>(a->g, a->outs, a->lo, x, y, z, v);
 }
 
 template <int D, int L, typename T>
-__device__ __noinline__ void write_images_noinline(const KArgs<T> a, int64_t x, int64_t y,
-                                                   int64_t z, const T* v) {
-  write_images<D, L>(a, x, y, z, v);
+__device__ __forceinline__ void images(const KArgs<T>& a, int64_t x, int64_t y, int64_t z,
+                                       const T* v) {
+  images_nl<D, L, T>(&a, x, y, z, v[0], v[1], v[2], v[3], D > 2 ? v[4] : T(0));
 }
 
 // ---------------------------------------------------------------------------
@@ -51,11 +57,11 @@ __device__ __noinline__ void write_images_noinline(const KArgs<T> a, int64_t x, 
 // evaluated (the simple, unfused baseline: 3 flux evaluations + 2 faces).
 // ---------------------------------------------------------------------------
 template <typename T, int D, int d, int L>
-__global__ void __launch_bounds__(256) k_sweep(const KArgs<T> a) {
+__global__ void __launch_bounds__(256) k_sweep(const __grid_constant__ KArgs<T> a) {
   constexpr int C = D + 2;
   const Geom& g = a.g;
   const int64_t n = g.cells();
-  bool ok = true;
+  int bad = 0, nan = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t x = i % g.S[0];
@@ -67,17 +73,18 @@ __global__ void __launch_bounds__(256) k_sweep(const KArgs<T> a) {
     load_cell<D, L>(g, a.in, x, y, z, U0);
     load_cell<D, L>(g, a.in, x + dm[0], y + dm[1], z + dm[2], Up);
     phys_flux<D, d>(Um, Fm, a.gm1);
-    ok &= phys_flux<D, d>(U0, F0, a.gm1);
+    bad |= phys_flux<D, d>(U0, F0, a.gm1);
     phys_flux<D, d>(Up, Fp, a.gm1);
     T PL[C], PR[C], o[C];
     force_face<D, d>(Um, Fm, U0, F0, PL, a.q[d], a.nq2[d], a.gm1);
     force_face<D, d>(U0, F0, Up, Fp, PR, a.q[d], a.nq2[d], a.gm1);
 #pragma unroll
     for (int c = 0; c < C; ++c) o[c] = U0[c] - (PR[c] - PL[c]);
+    nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
     store_cell<D, L>(g, a.out, x, y, z, o);
-    if (near_face<D>(g, x, y, z)) write_images_noinline<D, L>(a, x, y, z, o);
+    if (near_face<D>(g, x, y, z)) images<D, L>(a, x, y, z, o);
   }
-  if (!ok) atomicOr(a.flag, 1u);
+  if (bad < 0 || nan >= kExpMask<T>) atomicOr(a.flag, 1u);
 }
 
 // ---------------------------------------------------------------------------
@@ -85,128 +92,230 @@ __global__ void __launch_bounds__(256) k_sweep(const KArgs<T> a) {
 //
 // A warp owns a 64-slot window of one row (lane l holds slots 2l, 2l+1 as one
 // 128-bit (fp64) / 64-bit (fp32) vector; slot s <-> x = 62 w - 1 + s) and marches
-// down a chunk of `rows` rows.  For each row: vector-load U, x-sweep in
-// registers (face values shared across lanes with warp shuffles; slots 0 and 63
-// are the window's halo), then the y-face between this row and the previous
-// one from the march state (previous U*, F_y(U*), previous y-face), update and
-// store the previous row.  HBM traffic per cell: one read of U^n, one write of
-// U^{n+1}; the x-halo (2 of 64 slots) and the chunk's 2 halo rows are
-// recomputed, not re-stored.  Vector loads are 2-element aligned because the
-// layout puts x = -1 on an even element offset (geometry.hpp).
+// down a chunk of `rows` rows.  For each row: vector-load U (prefetched one row
+// ahead), x-sweep in registers (face values shared across lanes with warp
+// shuffles; slots 0 and 63 are the window's halo), then the y-face between this
+// row and the previous one from the march state (previous U*, F_y(U*), previous
+// y-face), update and store the previous row.  HBM traffic per cell: one read of
+// U^n, one write of U^{n+1}; the window's x-halo (2 of 64 slots) and the chunk's
+// 2 halo rows are recomputed, not re-stored.  Vector loads are aligned because
+// the layout puts x = -1 on an even element offset (geometry.hpp).
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(128) k_step2d(const KArgs<T> a, int nwin, int ntask) {
+struct Vert {  // y-march state of the lane's two cells (a, b)
+  T us[2][4];  // U* of the previous row
+  T fy[2][4];  // F_y(U*) of the previous row
+  T ph[2][4];  // previous y-face (scaled flux)
+};
+
+template <typename T>
+struct Ctx2 {  // loop-invariant per-lane data of k_step2d
+  const T* src;
+  T* dst;
+  int64_t rs, cp;
+  bool va, vb, ina, inb, xa_face, xb_face;
+  int64_t xa;
+  T gm1, qx, nqx, qy, nqy;
+  int pad, sy;
+};
+
+// x-sweep of the row held in u (lane's 2 cells), then F_y of the result.
+template <typename T>
+__device__ __forceinline__ void xsweep2(const Ctx2<T>& k, const typename Vec2<T>::type* u,
+                                        T (&S)[2][4], T (&G)[2][4], int& bad) {
+  constexpr int D = 2, C = 4;
+  T Ua[C], Ub[C], Fa[C], Fb[C], Pab[C], Pbn[C], Un[C], Fn[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    Ua[c] = u[c].x;
+    Ub[c] = u[c].y;
+  }
+  const int ba = phys_flux<D, 0>(Ua, Fa, k.gm1);
+  const int bb = phys_flux<D, 0>(Ub, Fb, k.gm1);
+  bad |= (k.ina ? ba : 0) | (k.inb ? bb : 0);
+  force_face<D, 0>(Ua, Fa, Ub, Fb, Pab, k.qx, k.nqx, k.gm1);
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    Un[c] = __shfl_down_sync(kFull, Ua[c], 1);
+    Fn[c] = __shfl_down_sync(kFull, Fa[c], 1);
+  }
+  force_face<D, 0>(Ub, Fb, Un, Fn, Pbn, k.qx, k.nqx, k.gm1);
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const T Ppa = __shfl_up_sync(kFull, Pbn[c], 1);
+    S[0][c] = Ua[c] - (Pab[c] - Ppa);
+    S[1][c] = Ub[c] - (Pbn[c] - Pab[c]);
+  }
+  const int ya = phys_flux<D, 1>(S[0], G[0], k.gm1);
+  const int yb = phys_flux<D, 1>(S[1], G[1], k.gm1);
+  bad |= (k.va ? ya : 0) | (k.vb ? yb : 0);
+}
+
+// One march step at row y (>= y0+1): x-sweep row y (already fetched into `cur`),
+// y-face y-1/2, update and store row y-1.
+template <typename T>
+__device__ __forceinline__ void march2(const KArgs<T>& a, const Ctx2<T>& k, int y, T* dst,
+                                       const typename Vec2<T>::type* cur, const Vert<T>& in,
+                                       Vert<T>& out, int& bad, int& nan) {
   constexpr int D = 2, C = 4;
   using V = typename Vec2<T>::type;
+  xsweep2(k, cur, out.us, out.fy, bad);
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    force_face<D, 1>(in.us[h], in.fy[h], out.us[h], out.fy[h], out.ph[h], k.qy, k.nqy, k.gm1);
+  T o[2][C];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < C; ++c) o[h][c] = in.us[h][c] - (out.ph[h][c] - in.ph[h][c]);
+  nan = max(nan, max(max(k.va ? naninf(o[0][0]) : 0, k.va ? naninf(o[0][3]) : 0),
+                     max(k.vb ? naninf(o[1][0]) : 0, k.vb ? naninf(o[1][3]) : 0)));
+  if (k.va & k.vb) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      V w;
+      w.x = o[0][c];
+      w.y = o[1][c];
+      *reinterpret_cast<V*>(dst + c * k.cp) = w;
+    }
+  } else {
+    if (k.va) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) dst[c * k.cp] = o[0][c];
+    }
+    if (k.vb) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) dst[c * k.cp + 1] = o[1][c];
+    }
+  }
+  const bool yface = (y - 1 < k.pad) | (y - 1 >= k.sy - k.pad);
+  if (k.va && (k.xa_face || yface)) images<D, 0>(a, k.xa, y - 1, 0, o[0]);
+  if (k.vb && (k.xb_face || yface)) images<D, 0>(a, k.xa + 1, y - 1, 0, o[1]);
+}
+
+// Per-warp ring of kNS row buffers filled by TMA bulk copies (cp.async.bulk):
+// each stage holds the window's 4 component sub-rows of one grid row; lane 0
+// refills a stage as soon as the warp has consumed it, so kNS-1 rows are in
+// flight while the warp computes (no prefetch registers).
+constexpr int kNS = 3;
+
+template <typename T>
+struct Ring2 {
+  static constexpr int RB = 64 * (int)sizeof(T) + 16;  // bytes per component sub-row
+  static constexpr int SB = 4 * RB;                    // bytes per stage
+  static constexpr int WB = kNS * SB + 64;             // bytes per warp (+ barriers)
+  unsigned char* buf;
+  uint64_t* bar;
+  const char* src0;  // 16-byte aligned global address of row y0-1, component 0
+  int64_t rowb, compb;  // bytes between rows / components
+  unsigned bytes;       // bytes per component copy
+  int shift;            // elements between the aligned start and slot 0
+  int krow_end;         // last row counter to fetch
+
+  __device__ __forceinline__ void issue(int kr) {  // lane 0 only
+    if (kr > krow_end) return;
+    const int s = kr % kNS;
+    const char* src = src0 + kr * rowb;
+    mbar_arrive_expect_tx(&bar[s], 4 * bytes);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) bulk_g2s(buf + s * SB + c * RB, src + c * compb, bytes, &bar[s]);
+  }
+  __device__ __forceinline__ void fetch(int kr, int lane, typename Vec2<T>::type* u) {
+    using V = typename Vec2<T>::type;
+    const int s = kr % kNS;
+    mbar_wait(&bar[s], (kr / kNS) & 1);
+    const unsigned char* b = buf + s * SB + (shift + 2 * lane) * (int)sizeof(T);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) u[c] = *reinterpret_cast<const V*>(b + c * RB);
+    __syncwarp();
+    if (lane == 0) {
+      fence_proxy_async();
+      issue(kr + kNS);
+    }
+  }
+};
+
+template <typename T, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_step2d(const __grid_constant__ KArgs<T> a, int nwin,
+                                                      int ntask) {
+  constexpr int D = 2, C = 4;
+  using V = typename Vec2<T>::type;
+  extern __shared__ __align__(128) unsigned char smem[];
   const Geom& g = a.g;
   const int lane = threadIdx.x & 31;
-  const int wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int wib = threadIdx.x >> 5;
+  const int wid = blockIdx.x * (blockDim.x >> 5) + wib;
   if (wid >= ntask) return;
   const int win = wid % nwin;
   const int chunk = wid / nwin;
-  const int64_t xa = (int64_t)win * kWinOut - 1 + 2 * lane;
-  const int64_t y0 = (int64_t)chunk * a.rows;
-  const int64_t y1 = min(y0 + (int64_t)a.rows, g.S[1]);
-  const int64_t cs = g.comp_stride, pitch = g.pitch;
-  const T* __restrict__ base = a.in + g.xo + xa;
-  T* __restrict__ obase = a.out + g.xo + xa;
-  const bool ina = (xa >= -1) & (xa <= g.S[0]);
-  const bool inb = (xa + 1 >= -1) & (xa + 1 <= g.S[0]);
-  const bool va = (lane >= 1) & (xa < g.S[0]);
-  const bool vb = (lane <= 30) & (xa + 1 < g.S[0]);
-  const T gm1 = a.gm1, qx = a.q[0], nqx = a.nq2[0], qy = a.q[1], nqy = a.nq2[1];
-  bool ok = true;
+  Ctx2<T> k;
+  const int64_t xw = (int64_t)win * kWinOut - 1;  // x of slot 0
+  k.xa = xw + 2 * lane;
+  const int y0 = chunk * a.rows;
+  const int y1 = min(y0 + a.rows, (int)g.S[1]);
+  k.rs = g.rstride;
+  k.cp = g.cstride;
+  k.va = (lane >= 1) & (k.xa < g.S[0]);
+  k.vb = (lane <= 30) & (k.xa + 1 < g.S[0]);
+  k.ina = (k.xa >= -1) & (k.xa <= g.S[0]);
+  k.inb = (k.xa + 1 >= -1) & (k.xa + 1 <= g.S[0]);
+  k.xa_face = k.va & ((k.xa < g.pad) | (k.xa >= g.S[0] - g.pad));
+  k.xb_face = k.vb & ((k.xa + 1 < g.pad) | (k.xa + 1 >= g.S[0] - g.pad));
+  k.gm1 = a.gm1;
+  k.qx = a.q[0];
+  k.nqx = a.nq2[0];
+  k.qy = a.q[1];
+  k.nqy = a.nq2[1];
+  k.pad = g.pad;
+  k.sy = (int)g.S[1];
 
-  T usA[C], fyA[C], phA[C], usB[C], fyB[C], phB[C];
-  V nxt[C];
-  {
-    const T* p = base + g.row(y0 - 1, 0) * pitch;
+  Ring2<T> ring;
+  ring.buf = smem + wib * Ring2<T>::WB;
+  ring.bar = reinterpret_cast<uint64_t*>(ring.buf + kNS * Ring2<T>::SB);
+  const T* w0 = a.in + g.row(y0 - 1, 0) * k.rs + g.xo + xw;
+  const uintptr_t mis = reinterpret_cast<uintptr_t>(w0) & 15;
+  ring.src0 = reinterpret_cast<const char*>(w0) - mis;
+  ring.shift = (int)(mis / sizeof(T));
+  ring.bytes = 64 * sizeof(T) + (mis ? 16 : 0);
+  ring.rowb = k.rs * (int64_t)sizeof(T);
+  ring.compb = k.cp * (int64_t)sizeof(T);
+  ring.krow_end = y1 - (y0 - 1);
+  if (lane == 0) {
 #pragma unroll
-    for (int c = 0; c < C; ++c) nxt[c] = *reinterpret_cast<const V*>(p + c * cs);
+    for (int s = 0; s < kNS; ++s) mbar_init(&ring.bar[s], 1);
+    fence_barrier_init();
+#pragma unroll
+    for (int s = 0; s < kNS; ++s) ring.issue(s);
   }
-  for (int64_t y = y0 - 1; y <= y1; ++y) {
-    T Ua[C], Ub[C];
+  __syncwarp();
+
+  T* dst = a.out + g.row(y0, 0) * k.rs + g.xo + k.xa;
+  int bad = 0, nan = 0;
+  // prologue: rows y0-1 and y0 (no update yet)
+  Vert<T> s0, s1;
+  V r[C];
+  ring.fetch(0, lane, r);
+  xsweep2(k, r, s0.us, s0.fy, bad);
+  ring.fetch(1, lane, r);
+  xsweep2(k, r, s1.us, s1.fy, bad);
 #pragma unroll
-    for (int c = 0; c < C; ++c) {
-      Ua[c] = nxt[c].x;
-      Ub[c] = nxt[c].y;
-    }
-    if (y < y1) {
-      const T* p = base + g.row(y + 1, 0) * pitch;
-#pragma unroll
-      for (int c = 0; c < C; ++c) nxt[c] = *reinterpret_cast<const V*>(p + c * cs);
-    }
-    // ---- x-sweep of row y
-    T Fa[C], Fb[C], Pab[C], Pbn[C], Un[C], Fn[C];
-    ok &= phys_flux<D, 0>(Ua, Fa, gm1) | !ina;
-    ok &= phys_flux<D, 0>(Ub, Fb, gm1) | !inb;
-    force_face<D, 0>(Ua, Fa, Ub, Fb, Pab, qx, nqx, gm1);
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      Un[c] = __shfl_down_sync(kFull, Ua[c], 1);
-      Fn[c] = __shfl_down_sync(kFull, Fa[c], 1);
-    }
-    force_face<D, 0>(Ub, Fb, Un, Fn, Pbn, qx, nqx, gm1);
-    T Sa[C], Sb[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      const T Ppa = __shfl_up_sync(kFull, Pbn[c], 1);
-      Sa[c] = Ua[c] - (Pab[c] - Ppa);
-      Sb[c] = Ub[c] - (Pbn[c] - Pab[c]);
-    }
-    // ---- y-sweep: face (y-1/2), update row y-1
-    T Ga[C], Gb[C];
-    ok &= phys_flux<D, 1>(Sa, Ga, gm1) | !va;
-    ok &= phys_flux<D, 1>(Sb, Gb, gm1) | !vb;
-    if (y >= y0) {
-      T Qa[C], Qb[C];
-      force_face<D, 1>(usA, fyA, Sa, Ga, Qa, qy, nqy, gm1);
-      force_face<D, 1>(usB, fyB, Sb, Gb, Qb, qy, nqy, gm1);
-      if (y > y0) {
-        T oa[C], ob[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          oa[c] = usA[c] - (Qa[c] - phA[c]);
-          ob[c] = usB[c] - (Qb[c] - phB[c]);
-        }
-        T* p = obase + g.row(y - 1, 0) * pitch;
-        if (va & vb) {
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            V w;
-            w.x = oa[c];
-            w.y = ob[c];
-            *reinterpret_cast<V*>(p + c * cs) = w;
-          }
-        } else {
-          if (va) {
-#pragma unroll
-            for (int c = 0; c < C; ++c) p[c * cs] = oa[c];
-          }
-          if (vb) {
-#pragma unroll
-            for (int c = 0; c < C; ++c) p[c * cs + 1] = ob[c];
-          }
-        }
-        if (va && near_face<D>(g, xa, y - 1, 0)) write_images_noinline<D, 0>(a, xa, y - 1, 0, oa);
-        if (vb && near_face<D>(g, xa + 1, y - 1, 0))
-          write_images_noinline<D, 0>(a, xa + 1, y - 1, 0, ob);
-      }
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        phA[c] = Qa[c];
-        phB[c] = Qb[c];
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      usA[c] = Sa[c];
-      fyA[c] = Ga[c];
-      usB[c] = Sb[c];
-      fyB[c] = Gb[c];
-    }
+  for (int h = 0; h < 2; ++h)
+    force_face<D, 1>(s0.us[h], s0.fy[h], s1.us[h], s1.fy[h], s1.ph[h], k.qy, k.nqy, k.gm1);
+  // steady state, two rows per iteration (state ping-pongs s1 -> s0 -> s1)
+  int y = y0 + 1;
+  for (; y + 1 <= y1; y += 2) {
+    ring.fetch(y - (y0 - 1), lane, r);
+    march2(a, k, y, dst, r, s1, s0, bad, nan);
+    dst += k.rs;
+    ring.fetch(y + 1 - (y0 - 1), lane, r);
+    march2(a, k, y + 1, dst, r, s0, s1, bad, nan);
+    dst += k.rs;
   }
-  if (!__all_sync(kFull, ok) && lane == 0) atomicOr(a.flag, 1u);
+  if (y <= y1) {
+    ring.fetch(y - (y0 - 1), lane, r);
+    march2(a, k, y, dst, r, s1, s0, bad, nan);
+  }
+  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
 }
 
 // ---------------------------------------------------------------------------
@@ -331,20 +440,29 @@ void launch_sweep(const KArgs<T>& a, int d, cudaStream_t s) {
 }
 
 int auto_rows_2d(const Geom& g) {
-  // aim for ~12 resident warps per SM over 148 SMs, march at least 8 rows
-  const int64_t target = 148 * 12;
+  // aim for ~16 resident warps per SM over 148 SMs, march at least 8 rows
+  const int64_t target = 148 * 16;
   int64_t rows = (g.S[1] * g.nwin + target - 1) / target;
   if (rows < 8) rows = 8;
   if (rows > g.S[1]) rows = g.S[1];
   return (int)rows;
 }
 
+int auto_rows_3d(const Geom& g) { return (int)(g.S[2] < 16 ? g.S[2] : 16); }
+
 template <typename T>
 void launch_step2d(const KArgs<T>& a, cudaStream_t s) {
   const int nchunk = (int)((a.g.S[1] + a.rows - 1) / a.rows);
   const int ntask = a.g.nwin * nchunk;
   const int wpb = 4;
-  k_step2d<T><<<(ntask + wpb - 1) / wpb, 32 * wpb, 0, s>>>(a, a.g.nwin, ntask);
+  const int grid = (ntask + wpb - 1) / wpb;
+  const int sm = wpb * Ring2<T>::WB;
+  // occupancy variant (min resident blocks of 128 threads per SM): register cap
+  // 128 / 168 / 255; default chosen by measurement
+  const int v = a.variant ? a.variant : 3;
+  if (v == 4) k_step2d<T, 4><<<grid, 32 * wpb, sm, s>>>(a, a.g.nwin, ntask);
+  else if (v == 2) k_step2d<T, 2><<<grid, 32 * wpb, sm, s>>>(a, a.g.nwin, ntask);
+  else k_step2d<T, 3><<<grid, 32 * wpb, sm, s>>>(a, a.g.nwin, ntask);
 }
 
 template <typename T>
@@ -381,8 +499,4 @@ template void launch_maxws<float>(const Geom&, const float*, double, unsigned lo
 template void launch_maxws<double>(const Geom&, const double*, double, unsigned long long*,
                                    unsigned*, cudaStream_t);
 
-}  // namespace rpl
-
-namespace rpl {
-int auto_rows_3d(const Geom& g) { return (int)(g.S[2] < 16 ? g.S[2] : 16); }
 }  // namespace rpl

@@ -67,8 +67,10 @@ int make_geom(int D, const int64_t size[3], int pad, const int parts[3], int ele
   if (g->xo + g->S[0] + pad > need) need = g->xo + g->S[0] + pad;
   const int64_t align = 128 / elem;
   g->pitch = (need + align - 1) / align * align;
-  g->comp_stride = g->pitch * g->P[1] * g->P[2];
-  g->buf_elems = (int64_t)g->C * g->comp_stride;
+  g->rstride = (int64_t)g->C * g->pitch;
+  g->cstride = layout == 0 ? g->pitch : 1;
+  g->xstride = layout == 0 ? 1 : g->C;
+  g->buf_elems = g->rstride * g->P[1] * g->P[2];
   return 0;
 }
 

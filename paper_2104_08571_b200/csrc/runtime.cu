@@ -8,6 +8,7 @@
 #include <nccl.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -132,9 +133,7 @@ __global__ void k_edge(const Geom g, const DevEdge e, T* buf, T* msg, int dir) {
       }
 #pragma unroll
       for (int c = 0; c < D + 2; ++c) {
-        const int64_t j = L == 0 ? c * g.comp_stride + g.row(s[1], s[2]) * g.pitch + g.xo + s[0]
-                                 : (g.row(s[1], s[2]) * g.pitch + g.xo + s[0]) * (D + 2) + c;
-        v[c] = buf[j];
+        v[c] = buf[g.at(c, s[0], s[1], s[2])];
       }
 #pragma unroll
       for (int d = 0; d < D; ++d)
@@ -161,7 +160,7 @@ __global__ void k_stage(const Geom g, T* buf, T* stage, int dir) {
     const int64_t x = i % g.S[0], y = (i / g.S[0]) % g.S[1], z = i / (g.S[0] * g.S[1]);
 #pragma unroll
     for (int c = 0; c < D + 2; ++c) {
-      const int64_t j = (g.row(y, z) * g.pitch + g.xo + x) * (D + 2) + c;
+      const int64_t j = g.at(c, x, y, z);
       if (dir == 0) buf[j] = stage[c * n + i];
       else stage[c * n + i] = buf[j];
     }
@@ -224,6 +223,7 @@ struct rpl_domain {
   void* d_send = nullptr;
   void* d_recv = nullptr;
   int rows = 0;
+  int variant = 0;  // RPL_VARIANT env: fused-kernel occupancy variant (tuning)
   // kernel timing (rpl_profile)
   std::vector<cudaEvent_t> ev;  // pairs
   size_t ev_used = 0;
@@ -274,7 +274,9 @@ extern "C" rpl_status rpl_config_check(const rpl_config* c) {
   return geom_of(c, &g);
 }
 
-static int64_t part_bytes(const Geom& g) { return round_up(g.buf_elems * g.elem, 256); }
+// + 512 B tail: the fused kernels' 16-byte-aligned bulk row copies may read up to
+// 16 B past the last row of a buffer (never used).
+static int64_t part_bytes(const Geom& g) { return round_up(g.buf_elems * g.elem + 512, 256); }
 
 extern "C" rpl_status rpl_arena_bytes(const rpl_config* c, size_t* out) {
   Geom g;
@@ -372,6 +374,7 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
   CU(cudaMallocHost(&d->h_flag, sizeof(unsigned)));
   CU(cudaMallocHost(&d->h_smax, sizeof(unsigned long long)));
   d->rows = c->rows_per_chunk;
+  if (const char* v = getenv("RPL_VARIANT")) d->variant = atoi(v);
   if (d->rows <= 0) d->rows = g.D == 2 ? auto_rows_2d(g) : (g.D == 3 ? auto_rows_3d(g) : 1);
   if (c->nranks > 1) {
     if (!g_nccl.load()) return fail(RPL_E_NCCL, "libnccl.so.2 not found (set RPL_NCCL_LIB)");
@@ -480,7 +483,7 @@ static rpl_status xfer(rpl_domain* d, void* host, bool to_dev) {
         memset(&m, 0, sizeof(m));
         cudaPitchedPtr hp = make_cudaPitchedPtr((char*)host + (size_t)c * bx * by * bz * el,
                                                 bx * el, bx * el, by);
-        cudaPitchedPtr dp = make_cudaPitchedPtr(dev + (size_t)c * g.comp_stride * el, g.pitch * el,
+        cudaPitchedPtr dp = make_cudaPitchedPtr(dev + (size_t)c * g.cstride * el, g.rstride * el,
                                                 g.pitch * el, g.P[1]);
         const cudaPos hpos = make_cudaPos(o[0] * el, o[1], o[2]);
         const cudaPos dpos = make_cudaPos(g.xo * el, g.off[1], g.off[2]);
@@ -658,6 +661,7 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps) {
   a.gm1 = (T)(d->cfg.gamma - 1.0);
   a.flag = d->d_flag;
   a.rows = d->rows;
+  a.variant = d->variant;
   const bool fused = use_fused(d);
   for (int s = 0; s < nsteps; ++s) {
     const int nsweep = fused ? 1 : g.D;
