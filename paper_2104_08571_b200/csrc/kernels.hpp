@@ -14,7 +14,10 @@ void launch_sweep(const KArgs<T>& a, int d, cudaStream_t s);      // K-A, one la
 template <typename T>
 void launch_step2d(const KArgs<T>& a, cudaStream_t s);            // K-B 2-D, one launch
 template <typename T>
-void launch_step3d(const KArgs<T>& a, cudaStream_t s);            // K-B 3-D, one launch
+int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s);  // K-B 3-D, one launch
+template <typename T>
+int make_tmap3d(const Geom& g, const void* buf, void* map_out);  // 128-byte CUtensorMap
+int window3d(const Geom& g);                                     // outputs per 3-D x-window
 template <typename T>
 void launch_fill(const Geom& g, int part, T* const* bufs, cudaStream_t s);
 template <typename T>

@@ -1,0 +1,331 @@
+// kernels3d.cu -- K-B (3-D): the x-, y- and z-sweeps of one step fused into one
+// HBM pass, TMA-staged.
+//
+// CTA tile: one x-window of W = 32V slots (lane l owns slots V l .. V l+V-1;
+// slot s <-> x = (W-2) w - 1 + s, slots 0 and W-1 are the x-halo), TY output rows
+// in y, and a chunk of z-planes that the CTA marches through (2.5-D streaming).
+// Warp j (0 <= j < TY+2) owns tile row y = y0 - 1 + j; warps 0 and TY+1 are the
+// y-halo rows.  Per z-plane:
+//   TMA   one elected thread streams whole plane tiles [TY+2 rows][C comps][W]
+//         into a 2-stage shared-memory ring (cp.async.bulk.tensor.4d, mbarrier
+//         completion), two planes ahead of the compute;
+//   X     every warp x-sweeps its row in registers (warp shuffles share faces),
+//         evaluates F_y of the result and publishes (U*, F_y) in shared memory;
+//   Y     warp j >= 1 computes the y-face between rows j-1 and j once and
+//         publishes it; warps 1..TY then update U** = U* - (Phi_{j+1/2} - Phi_{j-1/2});
+//   Z     warps 1..TY keep a z-march state per cell in registers (U** of the
+//         previous plane, its F_z and the previous z-face), compute the z-face,
+//         update and store plane z-1 (+ ghost images on partition faces).
+// Two __syncthreads per plane order the shared-memory hand-offs.  HBM traffic per
+// cell-step is one read of U^n (plus the tile halo, mostly L2 hits) and one write
+// of U^{n+1}; the halo rows/planes are recomputed, not re-stored.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "async.cuh"
+#include "kernels.hpp"
+#include "scheme.cuh"
+
+namespace rpl {
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int c, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(c), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int D, int L, typename T>
+__device__ __noinline__ void images3_nl(const KArgs<T>* a, int64_t x, int64_t y, int64_t z, T v0,
+                                        T v1, T v2, T v3, T v4) {
+  const T v[5] = {v0, v1, v2, v3, v4};
+  write_images<D, L>(a->g, a->outs, a->lo, x, y, z, v);
+}
+
+template <typename T, int V>
+struct ZState {
+  T us[V][5];  // U** of the previous plane
+  T fz[V][5];  // F_z(U**) of the previous plane
+  T ph[V][5];  // previous z-face
+};
+
+template <int TY, int V, typename T>
+struct Smem3 {
+  static constexpr int W = 32 * V, R = TY + 2, C = 5, NS = 2;
+  static constexpr int STAGE = R * C * W;           // elements per ring stage
+  static constexpr int XY = R * 2 * C * W;          // (U*, F_y) per tile row
+  static constexpr int FY = (R - 1) * C * W;        // y-faces
+  static constexpr size_t bytes() { return (size_t)(NS * STAGE + XY + FY) * sizeof(T) + 64; }
+};
+
+template <typename T, int V, int TY>
+__global__ void __launch_bounds__(32 * (TY + 2), 1)
+    k_step3d(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
+             int nwin, int nyb) {
+  constexpr int D = 3, C = 5, W = 32 * V, R = TY + 2;
+  using SM = Smem3<TY, V, T>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  T* stage = reinterpret_cast<T*>(smem);
+  T* xy = stage + SM::NS * SM::STAGE;
+  T* fyb = xy + SM::XY;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + SM::FY);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int t = blockIdx.x;
+  const int win = t % nwin;
+  t /= nwin;
+  const int yb = t % nyb;
+  const int zc = t / nyb;
+  const int xw = win * (W - 2) - 1;                 // x of slot 0
+  const int y0 = yb * TY;
+  const int z0 = zc * a.rows;
+  const int z1 = min(z0 + a.rows, (int)g.S[2]);
+  const int yr = y0 - 1 + warp;                     // this warp's row
+  const int SX = (int)g.S[0], SY = (int)g.S[1], SZ = (int)g.S[2];
+  // per-lane slot validity
+  int xs[V];
+  bool out_ok[V], in_ok[V], xface[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    xs[v] = xw + V * lane + v;
+    const int slot = V * lane + v;
+    out_ok[v] = (slot >= 1) & (slot <= W - 2) & (xs[v] < SX);
+    in_ok[v] = (xs[v] >= -1) & (xs[v] <= SX);
+    xface[v] = (xs[v] < g.pad) | (xs[v] >= SX - g.pad);
+  }
+  const bool row_in = yr <= SY;                      // row holds valid (interior/ghost) data
+  const bool row_out = (warp >= 1) & (warp <= TY) & (yr < SY);
+  const bool yface = (yr < g.pad) | (yr >= SY - g.pad);
+  const T gm1 = a.gm1;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < SM::NS; ++s) mbar_init(&bar[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int tx = (int)(g.xo + xw), ty = (int)(g.off[1] + y0 - 1);
+  const int nplanes = z1 - (z0 - 1) + 1;  // planes z0-1 .. z1
+  auto issue = [&](int kz) {
+    if (kz >= nplanes) return;
+    const int s = kz % SM::NS;
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
+    tma_load_4d(stage + s * SM::STAGE, &tmap, &bar[s], tx, 0, ty, (int)(g.off[2] + z0 - 1 + kz));
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < SM::NS; ++s) issue(s);
+  }
+
+  ZState<T, V> zs;
+  int bad = 0, nan = 0;
+  const T qx = a.q[0], nqx = a.nq2[0], qy = a.q[1], nqy = a.nq2[1], qz = a.q[2], nqz = a.nq2[2];
+  T* dst_row = a.out + g.row(yr, z0 - 1) * g.rstride + g.xo + xw + V * lane;
+  const int64_t plane = g.rstride * g.P[1];
+
+  for (int kz = 0; kz < nplanes; ++kz) {
+    const int z = z0 - 1 + kz;
+    const int s = kz % SM::NS;
+    mbar_wait(&bar[s], (kz / SM::NS) & 1);
+    // ---------------- X: this warp's row
+    T U[V][C], F[V][C], S_[V][C], G[V][C];
+    const T* st = stage + s * SM::STAGE + warp * C * W + V * lane;
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+#pragma unroll
+      for (int v = 0; v < V; ++v) U[v][c] = st[c * W + v];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int b = phys_flux<D, 0>(U[v], F[v], gm1);
+      bad |= (in_ok[v] & row_in) ? b : 0;
+    }
+    {
+      // faces: inside the lane (V == 2) and towards the next lane
+      T Pin[C], Pnx[C], Un[C], Fn[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Un[c] = __shfl_down_sync(0xffffffffu, U[0][c], 1);
+        Fn[c] = __shfl_down_sync(0xffffffffu, F[0][c], 1);
+      }
+      force_face<D, 0>(U[V - 1], F[V - 1], Un, Fn, Pnx, qx, nqx, gm1);
+      if (V == 2) force_face<D, 0>(U[0], F[0], U[V - 1], F[V - 1], Pin, qx, nqx, gm1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const T Ppv = __shfl_up_sync(0xffffffffu, Pnx[c], 1);
+        if (V == 2) {
+          S_[0][c] = U[0][c] - (Pin[c] - Ppv);
+          S_[V - 1][c] = U[V - 1][c] - (Pnx[c] - Pin[c]);
+        } else {
+          S_[0][c] = U[0][c] - (Pnx[c] - Ppv);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int b = phys_flux<D, 1>(S_[v], G[v], gm1);
+      bad |= (out_ok[v] & row_in) ? b : 0;
+    }
+    T* xr = xy + warp * 2 * C * W + V * lane;
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        xr[c * W + v] = S_[v][c];
+        xr[(C + c) * W + v] = G[v][c];
+      }
+    __syncthreads();  // (A): stage s consumed, (U*, F_y) published
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      issue(kz + SM::NS);
+    }
+    // ---------------- Y: face between rows warp-1 and warp
+    T Py[V][C];
+    if (warp >= 1) {
+      const T* pr = xy + (warp - 1) * 2 * C * W + V * lane;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        T Sp[C], Gp[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          Sp[c] = pr[c * W + v];
+          Gp[c] = pr[(C + c) * W + v];
+        }
+        force_face<D, 1>(Sp, Gp, S_[v], G[v], Py[v], qy, nqy, gm1);
+      }
+      T* fw = fyb + (warp - 1) * C * W + V * lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+#pragma unroll
+        for (int v = 0; v < V; ++v) fw[c * W + v] = Py[v][c];
+    }
+    __syncthreads();  // (B): y-faces published
+    // ---------------- Y update + Z march (rows 1..TY)
+    if (warp >= 1 && warp <= TY) {
+      const T* fu = fyb + warp * C * W + V * lane;  // face between warp and warp+1
+      T Us[V][C], Gz[V][C];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) Us[v][c] = S_[v][c] - (fu[c * W + v] - Py[v][c]);
+        const int b = phys_flux<D, 2>(Us[v], Gz[v], gm1);
+        bad |= (out_ok[v] & row_out) ? b : 0;
+      }
+      if (kz >= 1) {
+        T Pz[V][C];
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          force_face<D, 2>(zs.us[v], zs.fz[v], Us[v], Gz[v], Pz[v], qz, nqz, gm1);
+        if (kz >= 2) {
+          // update and store plane z-1
+          T o[V][C];
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+#pragma unroll
+            for (int c = 0; c < C; ++c) o[v][c] = zs.us[v][c] - (Pz[v][c] - zs.ph[v][c]);
+          T* dp = dst_row + (int64_t)(kz - 1) * plane;
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            if (out_ok[v] & row_out) {
+              nan = max(nan, max(naninf(o[v][0]), naninf(o[v][C - 1])));
+#pragma unroll
+              for (int c = 0; c < C; ++c) dp[c * g.cstride + v] = o[v][c];
+              const bool zf = (z - 1 < g.pad) | (z - 1 >= SZ - g.pad);
+              if (xface[v] | yface | zf)
+                images3_nl<D, 0, T>(&a, xs[v], yr, z - 1, o[v][0], o[v][1], o[v][2], o[v][3],
+                                    o[v][4]);
+            }
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+          for (int c = 0; c < C; ++c) zs.ph[v][c] = Pz[v][c];
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          zs.us[v][c] = Us[v][c];
+          zs.fz[v][c] = Gz[v][c];
+        }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// tile geometry per dtype: fp64 -> V = 1 (32-slot windows), fp32 -> V = 2
+template <typename T>
+struct Cfg3 {
+  static constexpr int V = sizeof(T) == 8 ? 1 : 2;
+  static constexpr int TY = 14;
+  static constexpr int W = 32 * V;
+};
+
+template <typename T>
+int make_tmap3d(const Geom& g, const void* buf, void* map_out) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return -1;
+  const cuuint64_t dims[4] = {(cuuint64_t)g.pitch, (cuuint64_t)g.C, (cuuint64_t)g.P[1],
+                              (cuuint64_t)g.P[2]};
+  const cuuint64_t strides[3] = {(cuuint64_t)(g.pitch * sizeof(T)),
+                                 (cuuint64_t)(g.rstride * sizeof(T)),
+                                 (cuuint64_t)(g.rstride * g.P[1] * sizeof(T))};
+  const cuuint32_t box[4] = {(cuuint32_t)Cfg3<T>::W, (cuuint32_t)g.C, (cuuint32_t)(Cfg3<T>::TY + 2),
+                             1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(map_out),
+                   sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                   4, const_cast<void*>(buf), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+int window3d(const Geom& g) { return g.elem == 8 ? 30 : 62; }
+
+template <typename T>
+int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  constexpr int V = Cfg3<T>::V, TY = Cfg3<T>::TY, W = Cfg3<T>::W;
+  const Geom& g = a.g;
+  const int nwin = (int)((g.S[0] + (W - 2) - 1) / (W - 2));
+  const int nyb = (int)((g.S[1] + TY - 1) / TY);
+  const int nzc = (int)((g.S[2] + a.rows - 1) / a.rows);
+  const size_t sm = Smem3<TY, V, T>::bytes();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_step3d<T, V, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  k_step3d<T, V, TY><<<nwin * nyb * nzc, 32 * (TY + 2), sm, s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb);
+  return 0;
+}
+
+template int make_tmap3d<float>(const Geom&, const void*, void*);
+template int make_tmap3d<double>(const Geom&, const void*, void*);
+template int launch_step3d<float>(const KArgs<float>&, const void*, cudaStream_t);
+template int launch_step3d<double>(const KArgs<double>&, const void*, cudaStream_t);
+
+}  // namespace rpl

@@ -223,7 +223,13 @@ struct rpl_domain {
   void* d_send = nullptr;
   void* d_recv = nullptr;
   int rows = 0;
-  int variant = 0;  // RPL_VARIANT env: fused-kernel occupancy variant (tuning)
+  int variant = 0;
+  // 3-D fused kernel: one TMA descriptor per (buffer, local partition)
+  struct alignas(64) TMap {
+    unsigned char b[128];
+  };
+  TMap tmap[2][kMaxParts];
+  bool tmaps_ok = false;  // RPL_VARIANT env: fused-kernel occupancy variant (tuning)
   // kernel timing (rpl_profile)
   std::vector<cudaEvent_t> ev;  // pairs
   size_t ev_used = 0;
@@ -373,6 +379,17 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
   CU(cudaMemsetAsync(d->d_flag, 0, sizeof(unsigned), d->stream));
   CU(cudaMallocHost(&d->h_flag, sizeof(unsigned)));
   CU(cudaMallocHost(&d->h_smax, sizeof(unsigned long long)));
+  if (g.D == 3 && g.layout == 0) {
+    d->tmaps_ok = true;
+    for (int p : d->local)
+      for (int b = 0; b < 2; ++b) {
+        const int r = g.elem == 8 ? make_tmap3d<double>(g, d->buf[b][p], d->tmap[b][p].b)
+                                  : make_tmap3d<float>(g, d->buf[b][p], d->tmap[b][p].b);
+        if (r != 0) d->tmaps_ok = false;
+      }
+    if (!d->tmaps_ok && c->kernel == RPL_KERNEL_FUSED)
+      return fail(RPL_E_CUDA, "cuTensorMapEncodeTiled failed for the 3-D fused kernel");
+  }
   d->rows = c->rows_per_chunk;
   if (const char* v = getenv("RPL_VARIANT")) d->variant = atoi(v);
   if (d->rows <= 0) d->rows = g.D == 2 ? auto_rows_2d(g) : (g.D == 3 ? auto_rows_3d(g) : 1);
@@ -633,7 +650,8 @@ extern "C" rpl_status rpl_fill_padding(rpl_domain* d) {
 }
 
 static bool use_fused(const rpl_domain* d) {
-  return d->cfg.kernel == RPL_KERNEL_FUSED && d->g.layout == 0 && d->g.D == 2;
+  return d->cfg.kernel == RPL_KERNEL_FUSED && d->g.layout == 0 &&
+         (d->g.D == 2 || (d->g.D == 3 && d->tmaps_ok));
 }
 
 extern "C" rpl_status rpl_launches_per_step(const rpl_domain* d, int32_t* out) {
@@ -676,7 +694,8 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps) {
         a.out = (T*)d->buf[nb][p];
         const bool prof = d->ev_used + 2 <= d->ev.size();
         if (prof) cudaEventRecord(d->ev[d->ev_used], d->stream);
-        if (fused) launch_step2d<T>(a, d->stream);
+        if (fused && g.D == 2) launch_step2d<T>(a, d->stream);
+        else if (fused) launch_step3d<T>(a, d->tmap[d->cur][p].b, d->stream);
         else launch_sweep<T>(a, sw, d->stream);
         if (prof) {
           cudaEventRecord(d->ev[d->ev_used + 1], d->stream);
