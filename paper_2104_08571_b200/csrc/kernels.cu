@@ -319,6 +319,183 @@ __global__ void __launch_bounds__(128, MINB) k_step2d(const __grid_constant__ KA
 }
 
 // ---------------------------------------------------------------------------
+// K-B (2-D), tile form: one CTA = one x-window (W = 32V slots, W-2 outputs) x
+// NW-2 output rows; warp j owns row y0-1+j (warps 0 and NW-1 are the y-halo).
+//   X  each warp loads its row (coalesced 64/128-bit vectors), x-sweeps it in
+//      registers (shuffles share faces), evaluates F_y and publishes (U*, F_y)
+//      in shared memory;
+//   Y  warp j >= 1 computes the y-face between rows j-1 and j once, publishes it;
+//      warps 1..NW-2 update and store.
+// No per-warp march: every warp does one row, so the SM holds many short,
+// independent warps (the fused step is latency-bound on long dependency chains
+// otherwise).  Recompute: the 2 halo rows per NW-2 rows and
+// the 2 halo slots per window.
+// ---------------------------------------------------------------------------
+template <typename T, int V>
+struct VecV;
+template <typename T>
+struct VecV<T, 1> {
+  using type = T;
+};
+template <typename T>
+struct VecV<T, 2> {
+  using type = typename Vec2<T>::type;
+};
+
+template <typename T, int V, int NW>
+__global__ void __launch_bounds__(32 * NW) k_step2d_tile(const __grid_constant__ KArgs<T> a,
+                                                         int nwin) {
+  constexpr int D = 2, C = 4, W = 32 * V;
+  using VT = typename VecV<T, V>::type;
+  __shared__ T xy[NW][2 * C][W];
+  __shared__ T fy[NW - 1][C][W];
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int win = blockIdx.x % nwin;
+  const int yb = blockIdx.x / nwin;
+  const int xw = win * (W - 2) - 1;
+  const int y0 = yb * (NW - 2);
+  const int yr = y0 - 1 + warp;
+  const int SX = (int)g.S[0], SY = (int)g.S[1];
+  const bool row_in = yr <= SY;  // rows -1..SY hold interior/ghost data
+  const bool row_out = (warp >= 1) & (warp <= NW - 2) & (yr < SY);
+  const T gm1 = a.gm1;
+  int xs[V];
+  bool out_ok[V], in_ok[V], xface[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    xs[v] = xw + V * lane + v;
+    const int slot = V * lane + v;
+    out_ok[v] = (slot >= 1) & (slot <= W - 2) & (xs[v] < SX);
+    in_ok[v] = (xs[v] >= -1) & (xs[v] <= SX);
+    xface[v] = (xs[v] < g.pad) | (xs[v] >= SX - g.pad);
+  }
+  int bad = 0, nan = 0;
+  // ---- X
+  T U[V][C], F[V][C], S_[V][C], G[V][C];
+  if (row_in) {
+    const T* src = a.in + g.row(yr, 0) * g.rstride + g.xo + xw + V * lane;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const VT u = *reinterpret_cast<const VT*>(src + c * g.cstride);
+      if constexpr (V == 1) {
+        U[0][c] = u;
+      } else {
+        U[0][c] = u.x;
+        U[1][c] = u.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int c = 0; c < C; ++c) U[v][c] = (c == 0 || c == C - 1) ? T(1) : T(0);
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int b = phys_flux<D, 0>(U[v], F[v], gm1);
+    bad |= (in_ok[v] & row_in) ? b : 0;
+  }
+  {
+    T Pin[C], Pnx[C], Un[C], Fn[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      Un[c] = __shfl_down_sync(kFull, U[0][c], 1);
+      Fn[c] = __shfl_down_sync(kFull, F[0][c], 1);
+    }
+    force_face<D, 0>(U[V - 1], F[V - 1], Un, Fn, Pnx, a.q[0], a.nq2[0], gm1);
+    if constexpr (V == 2) force_face<D, 0>(U[0], F[0], U[1], F[1], Pin, a.q[0], a.nq2[0], gm1);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const T Ppv = __shfl_up_sync(kFull, Pnx[c], 1);
+      if constexpr (V == 2) {
+        S_[0][c] = U[0][c] - (Pin[c] - Ppv);
+        S_[1][c] = U[1][c] - (Pnx[c] - Pin[c]);
+      } else {
+        S_[0][c] = U[0][c] - (Pnx[c] - Ppv);
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int b = phys_flux<D, 1>(S_[v], G[v], gm1);
+    bad |= (out_ok[v] & row_in) ? b : 0;
+  }
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      xy[warp][c][V * lane + v] = S_[v][c];
+      xy[warp][C + c][V * lane + v] = G[v][c];
+    }
+  __syncthreads();
+  // ---- Y face between rows warp-1 and warp
+  T Py[V][C];
+  if (warp >= 1) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      T Sp[C], Gp[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Sp[c] = xy[warp - 1][c][V * lane + v];
+        Gp[c] = xy[warp - 1][C + c][V * lane + v];
+      }
+      force_face<D, 1>(Sp, Gp, S_[v], G[v], Py[v], a.q[1], a.nq2[1], gm1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) fy[warp - 1][c][V * lane + v] = Py[v][c];
+    }
+  }
+  __syncthreads();
+  // ---- update + store
+  if (row_out) {
+    T* dst = a.out + g.row(yr, 0) * g.rstride + g.xo + xw + V * lane;
+    T o[V][C];
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+#pragma unroll
+      for (int c = 0; c < C; ++c) o[v][c] = S_[v][c] - (fy[warp][c][V * lane + v] - Py[v][c]);
+    const bool yface = (yr < g.pad) | (yr >= SY - g.pad);
+    if constexpr (V == 2) {
+      if (out_ok[0] & out_ok[1]) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          VT w;
+          w.x = o[0][c];
+          w.y = o[1][c];
+          *reinterpret_cast<VT*>(dst + c * g.cstride) = w;
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          if (out_ok[v])
+#pragma unroll
+            for (int c = 0; c < C; ++c) dst[c * g.cstride + v] = o[v][c];
+      }
+    } else {
+      if (out_ok[0])
+#pragma unroll
+        for (int c = 0; c < C; ++c) dst[c * g.cstride] = o[0][c];
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (out_ok[v]) {
+        nan = max(nan, max(naninf(o[v][0]), naninf(o[v][C - 1])));
+        if (xface[v] | yface) images<D, 0>(a, xs[v], yr, 0, o[v]);
+      }
+    }
+  }
+  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+}
+
+template <typename T, int V, int NW>
+static void launch_tile2d(const KArgs<T>& a, cudaStream_t s) {
+  constexpr int W = 32 * V;
+  const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
+  const int nyb = (int)((a.g.S[1] + (NW - 2) - 1) / (NW - 2));
+  k_step2d_tile<T, V, NW><<<nwin * nyb, 32 * NW, 0, s>>>(a, nwin);
+}
+
+// ---------------------------------------------------------------------------
 // Ghost fill of partition `part` from the current buffers of all partitions
 // (inverse of the image map: per dim, a ghost index maps to its source by the
 // boundary kind, interior indices of other partitions map to themselves).
@@ -469,7 +646,10 @@ void launch_step2d(const KArgs<T>& a, cudaStream_t s) {
   const int sm = wpb * Ring2<T>::WB;
   // occupancy variant (min resident blocks of 128 threads per SM): register cap
   // 128 / 168 / 255; default chosen by measurement
-  const int v = a.variant ? a.variant : 3;
+  const int v = a.variant;
+  if (v == 0 || v == 10) return launch_tile2d<T, 1, 16>(a, s);
+  if (v == 11) return launch_tile2d<T, 1, 8>(a, s);
+  if (v == 14) return launch_tile2d<T, 2, 8>(a, s);
   if (v == 4) k_step2d<T, 4><<<grid, 32 * wpb, sm, s>>>(a, a.g.nwin, ntask);
   else if (v == 2) k_step2d<T, 2><<<grid, 32 * wpb, sm, s>>>(a, a.g.nwin, ntask);
   else k_step2d<T, 3><<<grid, 32 * wpb, sm, s>>>(a, a.g.nwin, ntask);
