@@ -16,7 +16,7 @@ void launch_step2d(const KArgs<T>& a, cudaStream_t s);            // K-B 2-D, on
 template <typename T>
 int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s);  // K-B 3-D, one launch
 template <typename T>
-int make_tmap3d(const Geom& g, const void* buf, void* map_out);  // 128-byte CUtensorMap
+int make_tmap3d(const Geom& g, const void* buf, void* map_out, int variant);  // 128-byte CUtensorMap
 int window3d(const Geom& g);                                     // outputs per 3-D x-window
 template <typename T>
 void launch_fill(const Geom& g, int part, T* const* bufs, cudaStream_t s);

@@ -283,8 +283,13 @@ struct Cfg3 {
   static constexpr int W = 32 * V;
 };
 
+// x-window width of a 3-D launch (variant 20 forces V = 1 for fp32)
+static int win3(const Geom& g, int variant) {
+  return (g.elem == 8 || variant == 20) ? 32 : 64;
+}
+
 template <typename T>
-int make_tmap3d(const Geom& g, const void* buf, void* map_out) {
+int make_tmap3d(const Geom& g, const void* buf, void* map_out, int variant) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return -1;
   const cuuint64_t dims[4] = {(cuuint64_t)g.pitch, (cuuint64_t)g.C, (cuuint64_t)g.P[1],
@@ -292,8 +297,8 @@ int make_tmap3d(const Geom& g, const void* buf, void* map_out) {
   const cuuint64_t strides[3] = {(cuuint64_t)(g.pitch * sizeof(T)),
                                  (cuuint64_t)(g.rstride * sizeof(T)),
                                  (cuuint64_t)(g.rstride * g.P[1] * sizeof(T))};
-  const cuuint32_t box[4] = {(cuuint32_t)Cfg3<T>::W, (cuuint32_t)g.C, (cuuint32_t)(Cfg3<T>::TY + 2),
-                             1};
+  const cuuint32_t box[4] = {(cuuint32_t)win3(g, variant), (cuuint32_t)g.C,
+                             (cuuint32_t)(Cfg3<T>::TY + 2), 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(reinterpret_cast<CUtensorMap*>(map_out),
                    sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
@@ -305,9 +310,9 @@ int make_tmap3d(const Geom& g, const void* buf, void* map_out) {
 
 int window3d(const Geom& g) { return g.elem == 8 ? 30 : 62; }
 
-template <typename T>
-int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
-  constexpr int V = Cfg3<T>::V, TY = Cfg3<T>::TY, W = Cfg3<T>::W;
+template <typename T, int V>
+static int launch3(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  constexpr int TY = Cfg3<T>::TY, W = 32 * V;
   const Geom& g = a.g;
   const int nwin = (int)((g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((g.S[1] + TY - 1) / TY);
@@ -323,8 +328,14 @@ int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   return 0;
 }
 
-template int make_tmap3d<float>(const Geom&, const void*, void*);
-template int make_tmap3d<double>(const Geom&, const void*, void*);
+template <typename T>
+int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  if (sizeof(T) == 4 && a.variant == 20) return launch3<T, 1>(a, tmap, s);
+  return launch3<T, Cfg3<T>::V>(a, tmap, s);
+}
+
+template int make_tmap3d<float>(const Geom&, const void*, void*, int);
+template int make_tmap3d<double>(const Geom&, const void*, void*, int);
 template int launch_step3d<float>(const KArgs<float>&, const void*, cudaStream_t);
 template int launch_step3d<double>(const KArgs<double>&, const void*, cudaStream_t);
 

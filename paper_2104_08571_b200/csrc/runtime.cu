@@ -379,19 +379,19 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
   CU(cudaMemsetAsync(d->d_flag, 0, sizeof(unsigned), d->stream));
   CU(cudaMallocHost(&d->h_flag, sizeof(unsigned)));
   CU(cudaMallocHost(&d->h_smax, sizeof(unsigned long long)));
+  if (const char* v = getenv("RPL_VARIANT")) d->variant = atoi(v);
   if (g.D == 3 && g.layout == 0) {
     d->tmaps_ok = true;
     for (int p : d->local)
       for (int b = 0; b < 2; ++b) {
-        const int r = g.elem == 8 ? make_tmap3d<double>(g, d->buf[b][p], d->tmap[b][p].b)
-                                  : make_tmap3d<float>(g, d->buf[b][p], d->tmap[b][p].b);
+        const int r = g.elem == 8 ? make_tmap3d<double>(g, d->buf[b][p], d->tmap[b][p].b, d->variant)
+                                  : make_tmap3d<float>(g, d->buf[b][p], d->tmap[b][p].b, d->variant);
         if (r != 0) d->tmaps_ok = false;
       }
     if (!d->tmaps_ok && c->kernel == RPL_KERNEL_FUSED)
       return fail(RPL_E_CUDA, "cuTensorMapEncodeTiled failed for the 3-D fused kernel");
   }
   d->rows = c->rows_per_chunk;
-  if (const char* v = getenv("RPL_VARIANT")) d->variant = atoi(v);
   if (d->rows <= 0) d->rows = g.D == 2 ? auto_rows_2d(g) : (g.D == 3 ? auto_rows_3d(g) : 1);
   if (c->nranks > 1) {
     if (!g_nccl.load()) return fail(RPL_E_NCCL, "libnccl.so.2 not found (set RPL_NCCL_LIB)");
