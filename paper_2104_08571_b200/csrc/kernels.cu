@@ -8,6 +8,7 @@
 //                    then_reduce(Max)).
 // All step kernels write the ghost images of the cells they produce (scheme.cuh),
 // so no separate boundary or halo kernel runs between steps on one rank.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -496,6 +497,279 @@ static void launch_tile2d(const KArgs<T>& a, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
+// K-B (2-D), persistent TMA form (the default).  Same tile work as
+// k_step2d_tile, but each CTA loops over tiles and one elected thread streams
+// the next tiles' input boxes [NW rows][C comps][W slots] into a 2-stage
+// shared-memory ring with cp.async.bulk.tensor (TMA, mbarrier completion), so
+// HBM latency overlaps the previous tile's compute.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                             int x, int c, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(c), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename T, int V, int NW>
+struct SmemPT {
+  static constexpr int W = 32 * V, C = 4;
+  static constexpr int STAGE = NW * C * W;
+  static constexpr int XY = NW * 2 * C * W;
+  static constexpr int FY = (NW - 1) * C * W;
+  static constexpr size_t bytes() { return (size_t)(2 * STAGE + XY + FY) * sizeof(T) + 64; }
+};
+
+template <typename T, int V, int NW>
+__global__ void __launch_bounds__(32 * NW, (V == 1 ? 2 : 1))
+    k_step2d_pt(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
+                int nwin, int ntiles) {
+  constexpr int D = 2, C = 4, W = 32 * V;
+  using SM = SmemPT<T, V, NW>;
+  using VT = typename VecV<T, V>::type;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  T* stage = reinterpret_cast<T*>(smem);
+  T* xy = stage + 2 * SM::STAGE;
+  T* fy = xy + SM::XY;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fy + SM::FY);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int SX = (int)g.S[0], SY = (int)g.S[1];
+  const int G = gridDim.x;
+  const T gm1 = a.gm1, qx = a.q[0], nqx = a.nq2[0], qy = a.q[1], nqy = a.nq2[1];
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int i) {
+    const int tile = blockIdx.x + i * G;
+    if (tile >= ntiles) return;
+    const int s = i & 1;
+    const int w = tile % nwin, yb = tile / nwin;
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
+    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], (int)g.xo + w * (W - 2) - 1, 0,
+                 (int)g.off[1] + yb * (NW - 2) - 1, 0);
+  };
+  if (threadIdx.x == 0) {
+    issue(0);
+    issue(1);
+  }
+  int bad = 0, nan = 0;
+  for (int i = 0;; ++i) {
+    const int tile = blockIdx.x + i * G;
+    if (tile >= ntiles) break;
+    const int win = tile % nwin, yb = tile / nwin;
+    const int xw = win * (W - 2) - 1;
+    const int yr = yb * (NW - 2) - 1 + warp;
+    const bool row_in = yr <= SY;
+    const bool row_out = (warp >= 1) & (warp <= NW - 2) & (yr < SY);
+    const int s = i & 1;
+    mbar_wait(&bar[s], (i >> 1) & 1);
+    // ---- X
+    T U[V][C], F[V][C], S_[V][C], G_[V][C];
+    {
+      const T* st = stage + s * SM::STAGE + warp * C * W + V * lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const VT u = *reinterpret_cast<const VT*>(st + c * W);
+        if constexpr (V == 1) {
+          U[0][c] = u;
+        } else {
+          U[0][c] = u.x;
+          U[1][c] = u.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int xv = xw + V * lane + v;
+      const int b = phys_flux<D, 0>(U[v], F[v], gm1);
+      bad |= ((xv >= -1) & (xv <= SX) & row_in) ? b : 0;
+    }
+    {
+      T Pin[C], Pnx[C], Un[C], Fn[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Un[c] = __shfl_down_sync(kFull, U[0][c], 1);
+        Fn[c] = __shfl_down_sync(kFull, F[0][c], 1);
+      }
+      force_face<D, 0>(U[V - 1], F[V - 1], Un, Fn, Pnx, qx, nqx, gm1);
+      if constexpr (V == 2) force_face<D, 0>(U[0], F[0], U[1], F[1], Pin, qx, nqx, gm1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const T Ppv = __shfl_up_sync(kFull, Pnx[c], 1);
+        if constexpr (V == 2) {
+          S_[0][c] = U[0][c] - (Pin[c] - Ppv);
+          S_[1][c] = U[1][c] - (Pnx[c] - Pin[c]);
+        } else {
+          S_[0][c] = U[0][c] - (Pnx[c] - Ppv);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int xv = xw + V * lane + v;
+      const int slot = V * lane + v;
+      const int b = phys_flux<D, 1>(S_[v], G_[v], gm1);
+      bad |= ((slot >= 1) & (slot <= W - 2) & (xv < SX) & row_in) ? b : 0;
+    }
+    {
+      T* xr = xy + warp * 2 * C * W + V * lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        VT sv, gv;
+        if constexpr (V == 1) {
+          sv = S_[0][c];
+          gv = G_[0][c];
+        } else {
+          sv.x = S_[0][c];
+          sv.y = S_[1][c];
+          gv.x = G_[0][c];
+          gv.y = G_[1][c];
+        }
+        *reinterpret_cast<VT*>(xr + c * W) = sv;
+        *reinterpret_cast<VT*>(xr + (C + c) * W) = gv;
+      }
+    }
+    __syncthreads();  // (A) stage s consumed; (U*, F_y) published
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      issue(i + 2);
+    }
+    // ---- Y face between rows warp-1 and warp
+    T Py[V][C];
+    if (warp >= 1) {
+      const T* pr = xy + (warp - 1) * 2 * C * W + V * lane;
+      T Sp[V][C], Gp[V][C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const VT sv = *reinterpret_cast<const VT*>(pr + c * W);
+        const VT gv = *reinterpret_cast<const VT*>(pr + (C + c) * W);
+        if constexpr (V == 1) {
+          Sp[0][c] = sv;
+          Gp[0][c] = gv;
+        } else {
+          Sp[0][c] = sv.x;
+          Sp[1][c] = sv.y;
+          Gp[0][c] = gv.x;
+          Gp[1][c] = gv.y;
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) force_face<D, 1>(Sp[v], Gp[v], S_[v], G_[v], Py[v], qy, nqy, gm1);
+      T* fw = fy + (warp - 1) * C * W + V * lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        VT pv;
+        if constexpr (V == 1) {
+          pv = Py[0][c];
+        } else {
+          pv.x = Py[0][c];
+          pv.y = Py[1][c];
+        }
+        *reinterpret_cast<VT*>(fw + c * W) = pv;
+      }
+    }
+    __syncthreads();  // (B) y-faces published
+    // ---- update + store
+    if (row_out) {
+      T* dst = a.out + g.row(yr, 0) * g.rstride + g.xo + xw + V * lane;
+      const T* fu = fy + warp * C * W + V * lane;
+      T o[V][C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const VT pv = *reinterpret_cast<const VT*>(fu + c * W);
+        if constexpr (V == 1) {
+          o[0][c] = S_[0][c] - (pv - Py[0][c]);
+        } else {
+          o[0][c] = S_[0][c] - (pv.x - Py[0][c]);
+          o[1][c] = S_[1][c] - (pv.y - Py[1][c]);
+        }
+      }
+      bool ok[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int slot = V * lane + v;
+        ok[v] = (slot >= 1) & (slot <= W - 2) & (xw + slot < SX);
+      }
+      if constexpr (V == 2) {
+        if (ok[0] & ok[1]) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            VT w;
+            w.x = o[0][c];
+            w.y = o[1][c];
+            *reinterpret_cast<VT*>(dst + c * g.cstride) = w;
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            if (ok[v])
+#pragma unroll
+              for (int c = 0; c < C; ++c) dst[c * g.cstride + v] = o[v][c];
+        }
+      } else {
+        if (ok[0])
+#pragma unroll
+          for (int c = 0; c < C; ++c) dst[c * g.cstride] = o[0][c];
+      }
+      const bool yface = (yr < g.pad) | (yr >= SY - g.pad);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if (ok[v]) {
+          nan = max(nan, max(naninf(o[v][0]), naninf(o[v][C - 1])));
+          const int xv = xw + V * lane + v;
+          if (yface | (xv < g.pad) | (xv >= SX - g.pad)) images<D, 0>(a, xv, yr, 0, o[v]);
+        }
+      }
+    }
+  }
+  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+}
+
+template <typename T, int V, int NW>
+static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  constexpr int W = 32 * V;
+  using SM = SmemPT<T, V, NW>;
+  const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
+  const int nyb = (int)((a.g.S[1] + (NW - 2) - 1) / (NW - 2));
+  const int ntiles = nwin * nyb;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(k_step2d_pt<T, V, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SM::bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step2d_pt<T, V, NW>, 32 * NW,
+                                                  SM::bytes());
+    if (per_sm < 1) per_sm = 1;
+  }
+  int nsm = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int grid = per_sm * nsm;
+  if (grid > ntiles) grid = ntiles;
+  k_step2d_pt<T, V, NW><<<grid, 32 * NW, SM::bytes(), s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
+}
+
+// 2-D fused variants (RPL_VARIANT): 0/30 persistent TMA V=1 NW=16 (default),
+// 31 V=2 NW=8, 32 V=1 NW=8, 33 V=2 NW=16; 10/11/14 non-persistent tiles;
+// 2/3/4 per-warp march.  Box of the TMA variants:
+int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
+  (void)g;
+  switch (variant) {
+    case 0: case 30: *box_w = 32; *box_rows = 16; return 1;
+    case 31: *box_w = 64; *box_rows = 8; return 1;
+    case 32: *box_w = 32; *box_rows = 8; return 1;
+    case 33: *box_w = 64; *box_rows = 16; return 1;
+    default: return 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Ghost fill of partition `part` from the current buffers of all partitions
 // (inverse of the image map: per dim, a ghost index maps to its source by the
 // boundary kind, interior indices of other partitions map to themselves).
@@ -638,7 +912,14 @@ int auto_rows_3d(const Geom& g) {
 }
 
 template <typename T>
-void launch_step2d(const KArgs<T>& a, cudaStream_t s) {
+void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  switch (a.variant) {
+    case 0: case 30: return launch_pt2d<T, 1, 16>(a, tmap, s);
+    case 31: return launch_pt2d<T, 2, 8>(a, tmap, s);
+    case 32: return launch_pt2d<T, 1, 8>(a, tmap, s);
+    case 33: return launch_pt2d<T, 2, 16>(a, tmap, s);
+    default: break;
+  }
   const int nchunk = (int)((a.g.S[1] + a.rows - 1) / a.rows);
   const int ntask = a.g.nwin * nchunk;
   const int wpb = 4;
@@ -647,7 +928,7 @@ void launch_step2d(const KArgs<T>& a, cudaStream_t s) {
   // occupancy variant (min resident blocks of 128 threads per SM): register cap
   // 128 / 168 / 255; default chosen by measurement
   const int v = a.variant;
-  if (v == 0 || v == 10) return launch_tile2d<T, 1, 16>(a, s);
+  if (v == 10) return launch_tile2d<T, 1, 16>(a, s);
   if (v == 11) return launch_tile2d<T, 1, 8>(a, s);
   if (v == 14) return launch_tile2d<T, 2, 8>(a, s);
   if (v == 4) k_step2d<T, 4><<<grid, 32 * wpb, sm, s>>>(a, a.g.nwin, ntask);
@@ -680,8 +961,8 @@ void launch_maxws(const Geom& g, const T* in, double gamma, unsigned long long* 
 
 template void launch_sweep<float>(const KArgs<float>&, int, cudaStream_t);
 template void launch_sweep<double>(const KArgs<double>&, int, cudaStream_t);
-template void launch_step2d<float>(const KArgs<float>&, cudaStream_t);
-template void launch_step2d<double>(const KArgs<double>&, cudaStream_t);
+template void launch_step2d<float>(const KArgs<float>&, const void*, cudaStream_t);
+template void launch_step2d<double>(const KArgs<double>&, const void*, cudaStream_t);
 template void launch_fill<float>(const Geom&, int, float* const*, cudaStream_t);
 template void launch_fill<double>(const Geom&, int, double* const*, cudaStream_t);
 template void launch_maxws<float>(const Geom&, const float*, double, unsigned long long*,

@@ -12,11 +12,13 @@ struct KArgs;
 template <typename T>
 void launch_sweep(const KArgs<T>& a, int d, cudaStream_t s);      // K-A, one launch
 template <typename T>
-void launch_step2d(const KArgs<T>& a, cudaStream_t s);            // K-B 2-D, one launch
+void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s);  // K-B 2-D, one launch
 template <typename T>
 int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s);  // K-B 3-D, one launch
-template <typename T>
-int make_tmap3d(const Geom& g, const void* buf, void* map_out, int variant);  // 128-byte CUtensorMap
+int make_tmap3d(const Geom& g, const void* buf, void* map_out, int variant);
+// 4-D tensor map {pitch, C, P1, P2} of a SoA buffer with box {box_w, C, box_rows, 1}
+int make_tmap(const Geom& g, const void* buf, void* map_out, int box_w, int box_rows);
+int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows);  // 0 if 2-D uses TMA  // 128-byte CUtensorMap
 int window3d(const Geom& g);                                     // outputs per 3-D x-window
 template <typename T>
 void launch_fill(const Geom& g, int part, T* const* bufs, cudaStream_t s);

@@ -288,20 +288,17 @@ static int win3(const Geom& g, int variant) {
   return (g.elem == 8 || variant == 20) ? 32 : 64;
 }
 
-template <typename T>
-int make_tmap3d(const Geom& g, const void* buf, void* map_out, int variant) {
+int make_tmap(const Geom& g, const void* buf, void* map_out, int box_w, int box_rows) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return -1;
   const cuuint64_t dims[4] = {(cuuint64_t)g.pitch, (cuuint64_t)g.C, (cuuint64_t)g.P[1],
                               (cuuint64_t)g.P[2]};
-  const cuuint64_t strides[3] = {(cuuint64_t)(g.pitch * sizeof(T)),
-                                 (cuuint64_t)(g.rstride * sizeof(T)),
-                                 (cuuint64_t)(g.rstride * g.P[1] * sizeof(T))};
-  const cuuint32_t box[4] = {(cuuint32_t)win3(g, variant), (cuuint32_t)g.C,
-                             (cuuint32_t)(Cfg3<T>::TY + 2), 1};
+  const cuuint64_t strides[3] = {(cuuint64_t)(g.pitch * g.elem), (cuuint64_t)(g.rstride * g.elem),
+                                 (cuuint64_t)(g.rstride * g.P[1] * g.elem)};
+  const cuuint32_t box[4] = {(cuuint32_t)box_w, (cuuint32_t)g.C, (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(reinterpret_cast<CUtensorMap*>(map_out),
-                   sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                   g.elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                    4, const_cast<void*>(buf), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -334,8 +331,9 @@ int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   return launch3<T, Cfg3<T>::V>(a, tmap, s);
 }
 
-template int make_tmap3d<float>(const Geom&, const void*, void*, int);
-template int make_tmap3d<double>(const Geom&, const void*, void*, int);
+int make_tmap3d(const Geom& g, const void* buf, void* map_out, int variant) {
+  return make_tmap(g, buf, map_out, win3(g, variant), 14 + 2);
+}
 template int launch_step3d<float>(const KArgs<float>&, const void*, cudaStream_t);
 template int launch_step3d<double>(const KArgs<double>&, const void*, cudaStream_t);
 

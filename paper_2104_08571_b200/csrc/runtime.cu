@@ -384,12 +384,20 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
     d->tmaps_ok = true;
     for (int p : d->local)
       for (int b = 0; b < 2; ++b) {
-        const int r = g.elem == 8 ? make_tmap3d<double>(g, d->buf[b][p], d->tmap[b][p].b, d->variant)
-                                  : make_tmap3d<float>(g, d->buf[b][p], d->tmap[b][p].b, d->variant);
+        const int r = make_tmap3d(g, d->buf[b][p], d->tmap[b][p].b, d->variant);
         if (r != 0) d->tmaps_ok = false;
       }
     if (!d->tmaps_ok && c->kernel == RPL_KERNEL_FUSED)
       return fail(RPL_E_CUDA, "cuTensorMapEncodeTiled failed for the 3-D fused kernel");
+  }
+  {
+    int bw = 0, br = 0;
+    if (g.D == 2 && g.layout == 0 && tmap2d_box(g, d->variant, &bw, &br)) {
+      for (int p : d->local)
+        for (int b = 0; b < 2; ++b)
+          if (make_tmap(g, d->buf[b][p], d->tmap[b][p].b, bw, br) != 0)
+            return fail(RPL_E_CUDA, "cuTensorMapEncodeTiled failed for the 2-D fused kernel");
+    }
   }
   d->rows = c->rows_per_chunk;
   if (d->rows <= 0) d->rows = g.D == 2 ? auto_rows_2d(g) : (g.D == 3 ? auto_rows_3d(g) : 1);
@@ -694,7 +702,7 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps) {
         a.out = (T*)d->buf[nb][p];
         const bool prof = d->ev_used + 2 <= d->ev.size();
         if (prof) cudaEventRecord(d->ev[d->ev_used], d->stream);
-        if (fused && g.D == 2) launch_step2d<T>(a, d->stream);
+        if (fused && g.D == 2) launch_step2d<T>(a, d->tmap[d->cur][p].b, d->stream);
         else if (fused) launch_step3d<T>(a, d->tmap[d->cur][p].b, d->stream);
         else launch_sweep<T>(a, sw, d->stream);
         if (prof) {

@@ -1,9 +1,9 @@
 #!/bin/bash
-# Sweep fused 2-D kernel variants on one GPU (tuning; not a bench line).
 TAG=${1:-tune}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
-for v in 10 11 14 3; do
+timeout 300 python scripts/probe_f32.py > $OUT/probe_f32.txt 2>&1
+for v in 0 31 32 33 10; do
   RPL_VARIANT=$v timeout 120 python bench.py --steps 50 --no-cpu-baseline --e2e-steps 0 > $OUT/b_v${v}.json 2>>$OUT/err.log
 done
 OUT=$OUT python - <<'PY' > $OUT/summary.txt
@@ -15,7 +15,5 @@ for f in sorted(glob.glob(os.environ['OUT']+'/b_*.json')):
     except Exception as e: print(f, 'ERR', e)
 PY
 cat $OUT/summary.txt
-RPL_VARIANT=10 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_step2d -s 3 -c 1 \
-  -o $OUT/tile python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $OUT/ncu.log 2>&1
-bash scripts/dbg.sh $TAG
-timeout 900 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_step2d -s 3 -c 1 \
+  -o $OUT/pt python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $OUT/ncu.log 2>&1
