@@ -53,6 +53,7 @@ struct Geom {
   int64_t xstride;    // elements between consecutive x cells (SoA 1, AoS C)
   int64_t buf_elems;  // elements per partition buffer
   int nwin;           // fused: 62-cell windows per row
+  int img_fast;       // 1: single partition, pad <= 2, used extents >= 2 pad (images_single)
 
   // padded row index of (y, z) (signed interior coordinates)
   RPL_HD int64_t row(int64_t y, int64_t z) const { return (z + off[2]) * P[1] + (y + off[1]); }

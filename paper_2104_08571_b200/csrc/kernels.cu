@@ -50,6 +50,10 @@ __device__ __noinline__ void images_nl(const KArgs<T>* a, int64_t x, int64_t y, 
 template <int D, int L, typename T>
 __device__ __forceinline__ void images(const KArgs<T>& a, int64_t x, int64_t y, int64_t z,
                                        const T* v) {
+  if (L == 0 && a.g.img_fast) {
+    images_single<D>(a.g, a.out, (int)x, (int)y, (int)z, v);
+    return;
+  }
   images_nl<D, L, T>(&a, x, y, z, v[0], v[1], v[2], v[3], D > 2 ? v[4] : T(0));
 }
 
@@ -515,7 +519,11 @@ __device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map, 
 template <typename T, int V, int NW>
 struct SmemPT {
   static constexpr int W = 32 * V, C = 4;
-  static constexpr int STAGE = NW * C * W;
+  // TMA boxes must start 16-byte aligned in x: load AL extra elements from the
+  // aligned-down coordinate and skip `shift` of them when reading
+  static constexpr int AL = 16 / (int)sizeof(T);
+  static constexpr int WB = W + AL;
+  static constexpr int STAGE = NW * C * WB;
   static constexpr int XY = NW * 2 * C * W;
   static constexpr int FY = (NW - 1) * C * W;
   static constexpr size_t bytes() { return (size_t)(2 * STAGE + XY + FY) * sizeof(T) + 64; }
@@ -550,7 +558,8 @@ __global__ void __launch_bounds__(32 * NW, (V == 1 ? 2 : 1))
     const int s = i & 1;
     const int w = tile % nwin, yb = tile / nwin;
     mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
-    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], (int)g.xo + w * (W - 2) - 1, 0,
+    const int x0 = (int)g.xo + w * (W - 2) - 1;
+    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
                  (int)g.off[1] + yb * (NW - 2) - 1, 0);
   };
   if (threadIdx.x == 0) {
@@ -571,10 +580,11 @@ __global__ void __launch_bounds__(32 * NW, (V == 1 ? 2 : 1))
     // ---- X
     T U[V][C], F[V][C], S_[V][C], G_[V][C];
     {
-      const T* st = stage + s * SM::STAGE + warp * C * W + V * lane;
+      const int sh = ((int)g.xo + xw) % SM::AL;
+      const T* st = stage + s * SM::STAGE + warp * C * SM::WB + sh + V * lane;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        const VT u = *reinterpret_cast<const VT*>(st + c * W);
+        const VT u = *reinterpret_cast<const VT*>(st + c * SM::WB);
         if constexpr (V == 1) {
           U[0][c] = u;
         } else {
@@ -759,12 +769,12 @@ static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
 // 31 V=2 NW=8, 32 V=1 NW=8, 33 V=2 NW=16; 10/11/14 non-persistent tiles;
 // 2/3/4 per-warp march.  Box of the TMA variants:
 int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
-  (void)g;
+  const int al = 16 / g.elem;  // see SmemPT::AL
   switch (variant) {
-    case 0: case 30: *box_w = 32; *box_rows = 16; return 1;
-    case 31: *box_w = 64; *box_rows = 8; return 1;
-    case 32: *box_w = 32; *box_rows = 8; return 1;
-    case 33: *box_w = 64; *box_rows = 16; return 1;
+    case 0: case 30: *box_w = 32 + al; *box_rows = 16; return 1;
+    case 31: *box_w = 64 + al; *box_rows = 8; return 1;
+    case 32: *box_w = 32 + al; *box_rows = 8; return 1;
+    case 33: *box_w = 64 + al; *box_rows = 16; return 1;
     default: return 0;
   }
 }

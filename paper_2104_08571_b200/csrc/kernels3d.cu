@@ -55,7 +55,10 @@ struct ZState {
 template <int TY, int V, typename T>
 struct Smem3 {
   static constexpr int W = 32 * V, R = TY + 2, C = 5, NS = 2;
-  static constexpr int STAGE = R * C * W;           // elements per ring stage
+  // TMA boxes start 16-byte aligned in x: AL extra elements, read at `shift`
+  static constexpr int AL = 16 / (int)sizeof(T);
+  static constexpr int WB = W + AL;
+  static constexpr int STAGE = R * C * WB;          // elements per ring stage
   static constexpr int XY = R * 2 * C * W;          // (U*, F_y) per tile row
   static constexpr int FY = (R - 1) * C * W;        // y-faces
   static constexpr size_t bytes() { return (size_t)(NS * STAGE + XY + FY) * sizeof(T) + 64; }
@@ -107,7 +110,8 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1)
     fence_barrier_init();
   }
   __syncthreads();
-  const int tx = (int)(g.xo + xw), ty = (int)(g.off[1] + y0 - 1);
+  const int sh = (int)(g.xo + xw) % SM::AL;
+  const int tx = (int)(g.xo + xw) - sh, ty = (int)(g.off[1] + y0 - 1);
   const int nplanes = z1 - (z0 - 1) + 1;  // planes z0-1 .. z1
   auto issue = [&](int kz) {
     if (kz >= nplanes) return;
@@ -132,11 +136,11 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1)
     mbar_wait(&bar[s], (kz / SM::NS) & 1);
     // ---------------- X: this warp's row
     T U[V][C], F[V][C], S_[V][C], G[V][C];
-    const T* st = stage + s * SM::STAGE + warp * C * W + V * lane;
+    const T* st = stage + s * SM::STAGE + warp * C * SM::WB + sh + V * lane;
 #pragma unroll
     for (int c = 0; c < C; ++c)
 #pragma unroll
-      for (int v = 0; v < V; ++v) U[v][c] = st[c * W + v];
+      for (int v = 0; v < V; ++v) U[v][c] = st[c * SM::WB + v];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int b = phys_flux<D, 0>(U[v], F[v], gm1);
@@ -233,9 +237,13 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1)
 #pragma unroll
               for (int c = 0; c < C; ++c) dp[c * g.cstride + v] = o[v][c];
               const bool zf = (z - 1 < g.pad) | (z - 1 >= SZ - g.pad);
-              if (xface[v] | yface | zf)
-                images3_nl<D, 0, T>(&a, xs[v], yr, z - 1, o[v][0], o[v][1], o[v][2], o[v][3],
-                                    o[v][4]);
+              if (xface[v] | yface | zf) {
+                if (g.img_fast)
+                  images_single<D>(g, a.out, xs[v], yr, z - 1, o[v]);
+                else
+                  images3_nl<D, 0, T>(&a, xs[v], yr, z - 1, o[v][0], o[v][1], o[v][2], o[v][3],
+                                      o[v][4]);
+              }
             }
           }
         }
@@ -332,7 +340,7 @@ int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
 }
 
 int make_tmap3d(const Geom& g, const void* buf, void* map_out, int variant) {
-  return make_tmap(g, buf, map_out, win3(g, variant), 14 + 2);
+  return make_tmap(g, buf, map_out, win3(g, variant) + 16 / g.elem, 14 + 2);  // + Smem3::AL
 }
 template int launch_step3d<float>(const KArgs<float>&, const void*, cudaStream_t);
 template int launch_step3d<double>(const KArgs<double>&, const void*, cudaStream_t);

@@ -61,6 +61,9 @@ int make_geom(int D, const int64_t size[3], int pad, const int parts[3], int ele
   }
   if (g->nparts > kMaxParts) { *why = "too many partitions (max 64)"; return RPL_E_INVALID_ARG; }
   g->nwin = (int)((g->S[0] + kWinOut - 1) / kWinOut);
+  g->img_fast = (g->nparts == 1 && pad <= 2) ? 1 : 0;
+  for (int d = 0; d < D; ++d)
+    if (g->N[d] < 2 * pad) g->img_fast = 0;
   // x = -1 must sit on an even element offset: xo odd, xo >= pad
   g->xo = (pad % 2 == 1) ? pad : pad + 1;
   int64_t need = g->xo + (int64_t)kWinOut * g->nwin + 1;
