@@ -337,7 +337,7 @@ def main():
     value = global_cells * args.steps / t_total / 1e9
     peak, peak_src = measured_peak_gbs()
     alg_bytes = 2 * C * elem * local_cells  # per step-kernel launch (one partition per rank)
-    kname = {"fused": "k_step2d" if D == 2 else "k_sweep", "split": "k_sweep"}[args.kernel]
+    kname = {"fused": {1: "k_sweep", 2: "k_step2d_pt", 3: "k_step3d"}[D], "split": "k_sweep"}[args.kernel]
     per_launch_ms = kern_ms / max(kern_launches, 1)
     launches_per_step_kernel = max(1, kern_launches // args.steps)
     if args.kernel == "split" or D != 2:

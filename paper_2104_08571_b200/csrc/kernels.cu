@@ -765,15 +765,16 @@ static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
 }
 
-// 2-D fused variants (RPL_VARIANT): 0/30 persistent TMA V=1 NW=16 (default),
-// 31 V=2 NW=8, 32 V=1 NW=8, 33 V=2 NW=16; 10/11/14 non-persistent tiles;
+// 2-D fused variants (RPL_VARIANT): 0/32 persistent TMA V=1 NW=8 (default,
+// fastest measured), 30 V=1 NW=16, 31 V=2 NW=8, 33 V=2 NW=16;
+// 10/11/14 non-persistent tiles;
 // 2/3/4 per-warp march.  Box of the TMA variants:
 int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
   const int al = 16 / g.elem;  // see SmemPT::AL
   switch (variant) {
-    case 0: case 30: *box_w = 32 + al; *box_rows = 16; return 1;
+    case 30: *box_w = 32 + al; *box_rows = 16; return 1;
     case 31: *box_w = 64 + al; *box_rows = 8; return 1;
-    case 32: *box_w = 32 + al; *box_rows = 8; return 1;
+    case 0: case 32: *box_w = 32 + al; *box_rows = 8; return 1;
     case 33: *box_w = 64 + al; *box_rows = 16; return 1;
     default: return 0;
   }
@@ -924,9 +925,9 @@ int auto_rows_3d(const Geom& g) {
 template <typename T>
 void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   switch (a.variant) {
-    case 0: case 30: return launch_pt2d<T, 1, 16>(a, tmap, s);
+    case 30: return launch_pt2d<T, 1, 16>(a, tmap, s);
     case 31: return launch_pt2d<T, 2, 8>(a, tmap, s);
-    case 32: return launch_pt2d<T, 1, 8>(a, tmap, s);
+    case 0: case 32: return launch_pt2d<T, 1, 8>(a, tmap, s);
     case 33: return launch_pt2d<T, 2, 16>(a, tmap, s);
     default: break;
   }
