@@ -266,10 +266,16 @@ def main():
     C = D + 2
 
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush_rd = None if args.no_flush else torch.ones(32 << 20, dtype=torch.float64, device="cuda")
+    flush_acc = torch.zeros((), dtype=torch.float64, device="cuda")
 
     def do_flush():
+        # write 256 MiB (evicts the state from the 126 MB L2), then read another
+        # 256 MiB so the L2 holds clean lines: the next step pays no write-backs
+        # of the flush buffer
         if flush is not None:
             flush.fill_(1)
+            flush_acc.add_(flush_rd.sum())
 
     for _ in range(args.warmup):
         dom.advance(dt, 1)
@@ -285,6 +291,9 @@ def main():
     torch.cuda.synchronize()
     wall0 = time.perf_counter()
     with Clocks(dev) as clk:
+        # ~1 ms of GPU-side delay so the host can queue the timed steps ahead of
+        # the GPU: per-step events then measure device time, not launch latency
+        torch.cuda._sleep(2_000_000)
         for k in range(args.steps):
             ev[k][0].record(stream)
             dom.advance(dt, 1)

@@ -529,8 +529,8 @@ struct SmemPT {
   static constexpr size_t bytes() { return (size_t)(2 * STAGE + XY + FY) * sizeof(T) + 64; }
 };
 
-template <typename T, int V, int NW>
-__global__ void __launch_bounds__(32 * NW, (V == 1 ? 2 : 1))
+template <typename T, int V, int NW, int MB>
+__global__ void __launch_bounds__(32 * NW, MB)
     k_step2d_pt(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
                 int nwin, int ntiles) {
   constexpr int D = 2, C = 4, W = 32 * V;
@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(32 * NW, (V == 1 ? 2 : 1))
   if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
 }
 
-template <typename T, int V, int NW>
+template <typename T, int V, int NW, int MB = (V == 1 ? 2 : 1)>
 static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   constexpr int W = 32 * V;
   using SM = SmemPT<T, V, NW>;
@@ -749,9 +749,9 @@ static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   const int ntiles = nwin * nyb;
   static int per_sm = 0;
   if (!per_sm) {
-    cudaFuncSetAttribute(k_step2d_pt<T, V, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_step2d_pt<T, V, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)SM::bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step2d_pt<T, V, NW>, 32 * NW,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step2d_pt<T, V, NW, MB>, 32 * NW,
                                                   SM::bytes());
     if (per_sm < 1) per_sm = 1;
   }
@@ -761,7 +761,7 @@ static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   int grid = per_sm * nsm;
   if (grid > ntiles) grid = ntiles;
-  k_step2d_pt<T, V, NW><<<grid, 32 * NW, SM::bytes(), s>>>(
+  k_step2d_pt<T, V, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
 }
 
@@ -774,7 +774,8 @@ int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
   switch (variant) {
     case 30: *box_w = 32 + al; *box_rows = 16; return 1;
     case 31: *box_w = 64 + al; *box_rows = 8; return 1;
-    case 0: case 32: *box_w = 32 + al; *box_rows = 8; return 1;
+    case 0: case 32: case 34: case 35: *box_w = 32 + al; *box_rows = 8; return 1;
+    case 36: *box_w = 64 + al; *box_rows = 8; return 1;
     case 33: *box_w = 64 + al; *box_rows = 16; return 1;
     default: return 0;
   }
@@ -929,6 +930,9 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 31: return launch_pt2d<T, 2, 8>(a, tmap, s);
     case 0: case 32: return launch_pt2d<T, 1, 8>(a, tmap, s);
     case 33: return launch_pt2d<T, 2, 16>(a, tmap, s);
+    case 34: return launch_pt2d<T, 1, 8, 3>(a, tmap, s);
+    case 35: return launch_pt2d<T, 1, 8, 4>(a, tmap, s);
+    case 36: return launch_pt2d<T, 2, 8, 2>(a, tmap, s);
     default: break;
   }
   const int nchunk = (int)((a.g.S[1] + a.rows - 1) / a.rows);

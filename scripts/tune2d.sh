@@ -2,8 +2,8 @@
 TAG=${1:-tune}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
-timeout 300 python scripts/probe_f32.py > $OUT/probe_f32.txt 2>&1
-for v in 0 31 32 33 10; do
+
+for v in 0 34 35 36 31 33 10; do
   RPL_VARIANT=$v timeout 120 python bench.py --steps 50 --no-cpu-baseline --e2e-steps 0 > $OUT/b_v${v}.json 2>>$OUT/err.log
 done
 OUT=$OUT python - <<'PY' > $OUT/summary.txt
