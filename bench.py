@@ -293,7 +293,7 @@ def main():
     with Clocks(dev) as clk:
         # ~1 ms of GPU-side delay so the host can queue the timed steps ahead of
         # the GPU: per-step events then measure device time, not launch latency
-        torch.cuda._sleep(2_000_000)
+        torch.cuda._sleep(200_000 * args.steps)
         for k in range(args.steps):
             ev[k][0].record(stream)
             dom.advance(dt, 1)

@@ -765,6 +765,333 @@ static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
 }
 
+// ---------------------------------------------------------------------------
+// K-B (2-D), column-march form.  A work item is one x-window (W-2 outputs) x a
+// chunk of rows; the CTA marches down the chunk NW rows per step:
+//   X      warp j x-sweeps row k = NW t + j of the chunk (k = 0 is the row above
+//          the chunk) and publishes (U*, F_y) into a 2NW-row shared ring;
+//   Y      warp j computes the y-face between rows k-1 and k (row k-1 comes from
+//          the ring: the previous warp, or the previous step's last warp);
+//   update warp j updates row k with faces k (own) and k+1 (warp j+1); the last
+//          warp's update waits for the next step's first face (read back from
+//          the rings), so every row is x-swept once and every face computed once.
+// TMA streams the step boxes [NW rows][C][W+AL] into an NS-stage ring, NS-1
+// steps ahead, continuously across the CTA's work items (persistent grid).
+// ---------------------------------------------------------------------------
+template <typename T, int V, int NW>
+struct SmemCM {
+  static constexpr int W = 32 * V, C = 4, NS = 2;
+  static constexpr int AL = 16 / (int)sizeof(T);
+  static constexpr int WB = W + AL;
+  static constexpr int STAGE = NW * C * WB;
+  // ring depths (rows): U* of row k-1 is read again by the deferred update one
+  // step later -> 3 NW; F_y and faces are dead one step later -> 2 NW
+  static constexpr int RS = 3 * NW, RG = 2 * NW, RF = 2 * NW;
+  static constexpr int SR = RS * C * W, GR = RG * C * W, FR = RF * C * W;
+  static constexpr size_t bytes() { return (size_t)(NS * STAGE + SR + GR + FR) * sizeof(T) + 64; }
+};
+
+struct CMCursor {  // (work item, step) walker over this CTA's items
+  int i, t, nst, item;
+  __device__ __forceinline__ void set(int i_, int nwin, int chunk, int SY, int NW, int G,
+                                      int nwork) {
+    i = i_;
+    t = 0;
+    item = blockIdx.x + i * G;
+    nst = 0;
+    if (item < nwork) {
+      const int c = item / nwin;
+      const int y0 = c * chunk;
+      const int y1 = min(y0 + chunk, SY);
+      nst = (y1 - y0 + 2 + NW - 1) / NW;
+    }
+  }
+  __device__ __forceinline__ void next(int nwin, int chunk, int SY, int NW, int G, int nwork) {
+    if (++t >= nst) set(i + 1, nwin, chunk, SY, NW, G, nwork);
+  }
+};
+
+template <typename T, int V, int NW, int MB>
+__global__ void __launch_bounds__(32 * NW, MB)
+    k_step2d_cm(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
+                int nwin, int chunk, int nwork) {
+  constexpr int D = 2, C = 4, W = 32 * V;
+  using SM = SmemCM<T, V, NW>;
+  using VT = typename VecV<T, V>::type;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  T* stage = reinterpret_cast<T*>(smem);
+  T* sr = stage + SM::NS * SM::STAGE;
+  T* gr = sr + SM::SR;
+  T* fy = gr + SM::GR;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fy + SM::FR);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int SX = (int)g.S[0], SY = (int)g.S[1];
+  const int G = gridDim.x;
+  const T gm1 = a.gm1, qx = a.q[0], nqx = a.nq2[0], qy = a.q[1], nqy = a.nq2[1];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < SM::NS; ++s) mbar_init(&bar[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  // producer cursor (thread 0) runs NS-1 steps ahead of the consumers
+  CMCursor pc;
+  int pseq = 0;
+  auto issue_one = [&]() {
+    if (pc.item >= nwork) return;
+    const int s = pseq % SM::NS;
+    const int win = pc.item % nwin, c = pc.item / nwin;
+    const int x0 = (int)g.xo + win * (W - 2) - 1;
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
+    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
+                 (int)g.off[1] + c * chunk - 1 + NW * pc.t, 0);
+    ++pseq;
+    pc.next(nwin, chunk, SY, NW, G, nwork);
+  };
+  if (threadIdx.x == 0) {
+    pc.set(0, nwin, chunk, SY, NW, G, nwork);
+    for (int s = 0; s < SM::NS - 1; ++s) issue_one();
+  }
+  CMCursor cc;
+  cc.set(0, nwin, chunk, SY, NW, G, nwork);
+  int cseq = 0;
+  int bad = 0, nan = 0;
+  while (cc.item < nwork) {
+    const int win = cc.item % nwin, ch = cc.item / nwin;
+    const int y0 = ch * chunk;
+    const int y1 = min(y0 + chunk, SY);
+    const int xw = win * (W - 2) - 1;
+    const int sh = ((int)g.xo + xw) % SM::AL;
+    const int t = cc.t;
+    const int k = NW * t + warp;     // chunk-local row index, grid row y0 - 1 + k
+    const int yr = y0 - 1 + k;
+    const bool row_in = yr <= SY;
+    const int s = cseq % SM::NS;
+    mbar_wait(&bar[s], (cseq / SM::NS) & 1);
+    // ---- X
+    T U[V][C], F[V][C], S_[V][C], G_[V][C];
+    {
+      const T* st = stage + s * SM::STAGE + warp * C * SM::WB + sh + V * lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const VT u = *reinterpret_cast<const VT*>(st + c * SM::WB);
+        if constexpr (V == 1) {
+          U[0][c] = u;
+        } else {
+          U[0][c] = u.x;
+          U[1][c] = u.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int xv = xw + V * lane + v;
+      const int b = phys_flux<D, 0>(U[v], F[v], gm1);
+      bad |= ((xv >= -1) & (xv <= SX) & row_in) ? b : 0;
+    }
+    {
+      T Pin[C], Pnx[C], Un[C], Fn[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Un[c] = __shfl_down_sync(kFull, U[0][c], 1);
+        Fn[c] = __shfl_down_sync(kFull, F[0][c], 1);
+      }
+      force_face<D, 0>(U[V - 1], F[V - 1], Un, Fn, Pnx, qx, nqx, gm1);
+      if constexpr (V == 2) force_face<D, 0>(U[0], F[0], U[1], F[1], Pin, qx, nqx, gm1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const T Ppv = __shfl_up_sync(kFull, Pnx[c], 1);
+        if constexpr (V == 2) {
+          S_[0][c] = U[0][c] - (Pin[c] - Ppv);
+          S_[1][c] = U[1][c] - (Pnx[c] - Pin[c]);
+        } else {
+          S_[0][c] = U[0][c] - (Pnx[c] - Ppv);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int xv = xw + V * lane + v;
+      const int slot = V * lane + v;
+      const int b = phys_flux<D, 1>(S_[v], G_[v], gm1);
+      bad |= ((slot >= 1) & (slot <= W - 2) & (xv < SX) & row_in) ? b : 0;
+    }
+    {
+      T* sw = sr + (k % SM::RS) * C * W + V * lane;
+      T* gw = gr + (k % SM::RG) * C * W + V * lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        VT sv, gv;
+        if constexpr (V == 1) {
+          sv = S_[0][c];
+          gv = G_[0][c];
+        } else {
+          sv.x = S_[0][c];
+          sv.y = S_[1][c];
+          gv.x = G_[0][c];
+          gv.y = G_[1][c];
+        }
+        *reinterpret_cast<VT*>(sw + c * W) = sv;
+        *reinterpret_cast<VT*>(gw + c * W) = gv;
+      }
+    }
+    __syncthreads();  // (A): stage consumed, (U*, F_y) of this step published
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      issue_one();
+    }
+    // ---- Y: face k between rows k-1 and k
+    T Py[V][C];
+    if (k >= 1) {
+      const T* ps = sr + ((k - 1) % SM::RS) * C * W + V * lane;
+      const T* pg = gr + ((k - 1) % SM::RG) * C * W + V * lane;
+      T Sp[V][C], Gp[V][C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const VT sv = *reinterpret_cast<const VT*>(ps + c * W);
+        const VT gv = *reinterpret_cast<const VT*>(pg + c * W);
+        if constexpr (V == 1) {
+          Sp[0][c] = sv;
+          Gp[0][c] = gv;
+        } else {
+          Sp[0][c] = sv.x;
+          Sp[1][c] = sv.y;
+          Gp[0][c] = gv.x;
+          Gp[1][c] = gv.y;
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) force_face<D, 1>(Sp[v], Gp[v], S_[v], G_[v], Py[v], qy, nqy, gm1);
+      T* fw = fy + (k % SM::RF) * C * W + V * lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        VT pv;
+        if constexpr (V == 1) {
+          pv = Py[0][c];
+        } else {
+          pv.x = Py[0][c];
+          pv.y = Py[1][c];
+        }
+        *reinterpret_cast<VT*>(fw + c * W) = pv;
+      }
+    }
+    __syncthreads();  // (B): faces of this step published
+    // ---- updates: warp j < NW-1 updates its own row k (faces k and k+1);
+    // warp 0 also completes the previous step's last row (k-1) from the rings.
+    auto update_store = [&](int kk, const T (*Sv)[C], const T (*Pl)[C], const T* fup) {
+      const int yy = y0 - 1 + kk;
+      if (kk < 1 || yy >= y1) return;
+      T* dst = a.out + g.row(yy, 0) * g.rstride + g.xo + xw + V * lane;
+      T o[V][C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const VT pv = *reinterpret_cast<const VT*>(fup + c * W);
+        if constexpr (V == 1) {
+          o[0][c] = Sv[0][c] - (pv - Pl[0][c]);
+        } else {
+          o[0][c] = Sv[0][c] - (pv.x - Pl[0][c]);
+          o[1][c] = Sv[1][c] - (pv.y - Pl[1][c]);
+        }
+      }
+      bool ok[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int slot = V * lane + v;
+        ok[v] = (slot >= 1) & (slot <= W - 2) & (xw + slot < SX);
+      }
+      if constexpr (V == 2) {
+        if (ok[0] & ok[1]) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            VT w;
+            w.x = o[0][c];
+            w.y = o[1][c];
+            *reinterpret_cast<VT*>(dst + c * g.cstride) = w;
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            if (ok[v])
+#pragma unroll
+              for (int c = 0; c < C; ++c) dst[c * g.cstride + v] = o[v][c];
+        }
+      } else {
+        if (ok[0])
+#pragma unroll
+          for (int c = 0; c < C; ++c) dst[c * g.cstride] = o[0][c];
+      }
+      const bool yface = (yy < g.pad) | (yy >= SY - g.pad);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if (ok[v]) {
+          nan = max(nan, max(naninf(o[v][0]), naninf(o[v][C - 1])));
+          const int xv = xw + V * lane + v;
+          if (yface | (xv < g.pad) | (xv >= SX - g.pad)) images<D, 0>(a, xv, yy, 0, o[v]);
+        }
+      }
+    };
+    // (the last warp's row of a chunk's final step is never an output row)
+    if (warp < NW - 1) update_store(k, S_, Py, fy + ((k + 1) % SM::RF) * C * W + V * lane);
+    if (warp == 0 && t >= 1) {
+      // previous step's last row kp = k - 1 (warp NW-1 of step t-1): U* and its lower
+      // face from the rings, upper face = this warp's face k
+      const int kp = k - 1;
+      const T* pr = sr + (kp % SM::RS) * C * W + V * lane;
+      const T* pl = fy + (kp % SM::RF) * C * W + V * lane;
+      T Sv[V][C], Pl[V][C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const VT sv = *reinterpret_cast<const VT*>(pr + c * W);
+        const VT lv = *reinterpret_cast<const VT*>(pl + c * W);
+        if constexpr (V == 1) {
+          Sv[0][c] = sv;
+          Pl[0][c] = lv;
+        } else {
+          Sv[0][c] = sv.x;
+          Sv[1][c] = sv.y;
+          Pl[0][c] = lv.x;
+          Pl[1][c] = lv.y;
+        }
+      }
+      update_store(kp, Sv, Pl, fy + (k % SM::RF) * C * W + V * lane);
+    }
+    ++cseq;
+    cc.next(nwin, chunk, SY, NW, G, nwork);
+  }
+  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+}
+
+template <typename T, int V, int NW, int MB>
+static void launch_cm2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  constexpr int W = 32 * V;
+  using SM = SmemCM<T, V, NW>;
+  const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(k_step2d_cm<T, V, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SM::bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step2d_cm<T, V, NW, MB>, 32 * NW,
+                                                  SM::bytes());
+    if (per_sm < 1) per_sm = 1;
+  }
+  int nsm = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int resident = per_sm * nsm;
+  // chunk rows: ~2 work items per resident CTA, a multiple of NW, >= 2 NW
+  const int64_t SY = a.g.S[1];
+  int64_t chunk = (SY * nwin + 2 * resident - 1) / (2 * resident);
+  chunk = (chunk + NW - 1) / NW * NW;
+  if (chunk < 2 * NW) chunk = 2 * NW;
+  if (a.rows > 0) chunk = a.rows;
+  const int nchunk = (int)((SY + chunk - 1) / chunk);
+  const int nwork = nwin * nchunk;
+  const int grid = nwork < resident ? nwork : resident;
+  k_step2d_cm<T, V, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, (int)chunk, nwork);
+}
+
 // 2-D fused variants (RPL_VARIANT): 0/32 persistent TMA V=1 NW=8 (default,
 // fastest measured), 30 V=1 NW=16, 31 V=2 NW=8, 33 V=2 NW=16;
 // 10/11/14 non-persistent tiles;
@@ -776,6 +1103,9 @@ int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
     case 31: *box_w = 64 + al; *box_rows = 8; return 1;
     case 0: case 32: case 34: case 35: *box_w = 32 + al; *box_rows = 8; return 1;
     case 36: *box_w = 64 + al; *box_rows = 8; return 1;
+    case 40: case 41: *box_w = 32 + al; *box_rows = 8; return 1;
+    case 42: *box_w = 64 + al; *box_rows = 8; return 1;
+    case 43: *box_w = 32 + al; *box_rows = 16; return 1;
     case 33: *box_w = 64 + al; *box_rows = 16; return 1;
     default: return 0;
   }
@@ -931,6 +1261,10 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 0: case 32: return launch_pt2d<T, 1, 8>(a, tmap, s);
     case 33: return launch_pt2d<T, 2, 16>(a, tmap, s);
     case 34: return launch_pt2d<T, 1, 8, 3>(a, tmap, s);
+    case 40: return launch_cm2d<T, 1, 8, 3>(a, tmap, s);
+    case 41: return launch_cm2d<T, 1, 8, 2>(a, tmap, s);
+    case 42: return launch_cm2d<T, 2, 8, 2>(a, tmap, s);
+    case 43: return launch_cm2d<T, 1, 16, 1>(a, tmap, s);
     case 35: return launch_pt2d<T, 1, 8, 4>(a, tmap, s);
     case 36: return launch_pt2d<T, 2, 8, 2>(a, tmap, s);
     default: break;

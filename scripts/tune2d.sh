@@ -2,8 +2,10 @@
 TAG=${1:-tune}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
-
-for v in 0 34 35 36 31 33 10; do
+for v in 40 42; do
+  RPL_VARIANT=$v timeout 600 python -m pytest tests -m gpu -q -x -k "2d or partitioned or split_fused or ghosts_after or smoke or full_size" > $OUT/pytest_v$v.log 2>&1; echo "rc=$?" >> $OUT/pytest_v$v.log
+done
+for v in 34 40 41 42 43; do
   RPL_VARIANT=$v timeout 120 python bench.py --steps 50 --no-cpu-baseline --e2e-steps 0 > $OUT/b_v${v}.json 2>>$OUT/err.log
 done
 OUT=$OUT python - <<'PY' > $OUT/summary.txt
@@ -11,9 +13,10 @@ import json,glob,os
 for f in sorted(glob.glob(os.environ['OUT']+'/b_*.json')):
     try:
         d=json.loads(open(f).read().strip().splitlines()[-1])
-        print(os.path.basename(f), round(d['value'],1), 'Gcell/s', round(d['roofline']['launch_ms']*1e3,2),'us', round(d['roofline']['frac'],3))
+        print(os.path.basename(f), round(d['value'],1), 'Gcell/s', round(d['ms_per_step']*1e3,2), 'us/step', round(d['roofline']['launch_ms']*1e3,2),'us', round(d['roofline']['frac'],3))
     except Exception as e: print(f, 'ERR', e)
 PY
 cat $OUT/summary.txt
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_step2d -s 3 -c 1 \
-  -o $OUT/pt python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $OUT/ncu.log 2>&1
+tail -2 $OUT/pytest_v40.log $OUT/pytest_v42.log
+RPL_VARIANT=40 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_step2d -s 3 -c 1 \
+  -o $OUT/cm python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $OUT/ncu.log 2>&1
