@@ -1244,7 +1244,7 @@ int auto_rows_2d(const Geom& g) {
 int auto_rows_3d(const Geom& g) {
   // z-planes per CTA: enough CTAs for ~6 waves of 148, at least 8 planes per march
   const int64_t ww = window3d(g);
-  const int64_t tiles = ((g.S[0] + ww - 1) / ww) * ((g.S[1] + 13) / 14);
+  const int64_t tiles = ((g.S[0] + ww - 1) / ww) * ((g.S[1] + 13) / 14);  // (TY = 14 estimate)
   int64_t nzc = (148 * 6 + tiles - 1) / tiles;
   if (nzc < 1) nzc = 1;
   int64_t rows = (g.S[2] + nzc - 1) / nzc;

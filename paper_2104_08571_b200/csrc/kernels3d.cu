@@ -292,6 +292,9 @@ struct Cfg3 {
   static constexpr int W = 32 * V;
 };
 
+// tile rows of a 3-D launch (variants 50: 30 rows, 51: 22 rows; default 14)
+static int ty3(int variant) { return variant == 50 ? 30 : (variant == 51 ? 22 : 14); }
+
 // x-window width of a 3-D launch (variant 21: fp32 with V = 2)
 static int win3(const Geom& g, int variant) {
   return (g.elem == 4 && variant == 21) ? 64 : 32;
@@ -316,9 +319,9 @@ int make_tmap(const Geom& g, const void* buf, void* map_out, int box_w, int box_
 
 int window3d(const Geom& g) { return 30; }
 
-template <typename T, int V>
+template <typename T, int V, int TY>
 static int launch3(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
-  constexpr int TY = Cfg3<T>::TY, W = 32 * V;
+  constexpr int W = 32 * V;
   const Geom& g = a.g;
   const int nwin = (int)((g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((g.S[1] + TY - 1) / TY);
@@ -336,12 +339,17 @@ static int launch3(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
 
 template <typename T>
 int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
-  if (sizeof(T) == 4 && a.variant == 21) return launch3<T, 2>(a, tmap, s);
-  return launch3<T, 1>(a, tmap, s);
+  switch (a.variant) {
+    case 21: return launch3<T, 2, 14>(a, tmap, s);
+    case 50: return launch3<T, 1, 30>(a, tmap, s);
+    case 51: return launch3<T, 1, 22>(a, tmap, s);
+    default: return launch3<T, 1, 14>(a, tmap, s);
+  }
 }
 
 int make_tmap3d(const Geom& g, const void* buf, void* map_out, int variant) {
-  return make_tmap(g, buf, map_out, win3(g, variant) + 16 / g.elem, 14 + 2);  // + Smem3::AL
+  return make_tmap(g, buf, map_out, win3(g, variant) + 16 / g.elem,  // + Smem3::AL
+                   ty3(variant) + 2);
 }
 template int launch_step3d<float>(const KArgs<float>&, const void*, cudaStream_t);
 template int launch_step3d<double>(const KArgs<double>&, const void*, cudaStream_t);
