@@ -865,6 +865,9 @@ __global__ void __launch_bounds__(32 * NW, MB)
     const int sh = ((int)g.xo + xw) % SM::AL;
     const int t = cc.t;
     const int k = NW * t + warp;     // chunk-local row index, grid row y0 - 1 + k
+    // ring row: keeps increasing across work items, so ring slots are only
+    // reused after the barriers that order their last reads (NW * cseq + warp)
+    const int kr = NW * cseq + warp;
     const int yr = y0 - 1 + k;
     const bool row_in = yr <= SY;
     const int s = cseq % SM::NS;
@@ -918,8 +921,8 @@ __global__ void __launch_bounds__(32 * NW, MB)
       bad |= ((slot >= 1) & (slot <= W - 2) & (xv < SX) & row_in) ? b : 0;
     }
     {
-      T* sw = sr + (k % SM::RS) * C * W + V * lane;
-      T* gw = gr + (k % SM::RG) * C * W + V * lane;
+      T* sw = sr + (kr % SM::RS) * C * W + V * lane;
+      T* gw = gr + (kr % SM::RG) * C * W + V * lane;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         VT sv, gv;
@@ -944,8 +947,8 @@ __global__ void __launch_bounds__(32 * NW, MB)
     // ---- Y: face k between rows k-1 and k
     T Py[V][C];
     if (k >= 1) {
-      const T* ps = sr + ((k - 1) % SM::RS) * C * W + V * lane;
-      const T* pg = gr + ((k - 1) % SM::RG) * C * W + V * lane;
+      const T* ps = sr + ((kr - 1) % SM::RS) * C * W + V * lane;
+      const T* pg = gr + ((kr - 1) % SM::RG) * C * W + V * lane;
       T Sp[V][C], Gp[V][C];
 #pragma unroll
       for (int c = 0; c < C; ++c) {
@@ -963,7 +966,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
       }
 #pragma unroll
       for (int v = 0; v < V; ++v) force_face<D, 1>(Sp[v], Gp[v], S_[v], G_[v], Py[v], qy, nqy, gm1);
-      T* fw = fy + (k % SM::RF) * C * W + V * lane;
+      T* fw = fy + (kr % SM::RF) * C * W + V * lane;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         VT pv;
@@ -1032,13 +1035,13 @@ __global__ void __launch_bounds__(32 * NW, MB)
       }
     };
     // (the last warp's row of a chunk's final step is never an output row)
-    if (warp < NW - 1) update_store(k, S_, Py, fy + ((k + 1) % SM::RF) * C * W + V * lane);
+    if (warp < NW - 1) update_store(k, S_, Py, fy + ((kr + 1) % SM::RF) * C * W + V * lane);
     if (warp == 0 && t >= 1) {
       // previous step's last row kp = k - 1 (warp NW-1 of step t-1): U* and its lower
       // face from the rings, upper face = this warp's face k
       const int kp = k - 1;
-      const T* pr = sr + (kp % SM::RS) * C * W + V * lane;
-      const T* pl = fy + (kp % SM::RF) * C * W + V * lane;
+      const T* pr = sr + ((kr - 1) % SM::RS) * C * W + V * lane;
+      const T* pl = fy + ((kr - 1) % SM::RF) * C * W + V * lane;
       T Sv[V][C], Pl[V][C];
 #pragma unroll
       for (int c = 0; c < C; ++c) {
@@ -1054,7 +1057,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
           Pl[1][c] = lv.y;
         }
       }
-      update_store(kp, Sv, Pl, fy + (k % SM::RF) * C * W + V * lane);
+      update_store(kp, Sv, Pl, fy + (kr % SM::RF) * C * W + V * lane);
     }
     ++cseq;
     cc.next(nwin, chunk, SY, NW, G, nwork);
@@ -1269,7 +1272,9 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 36: return launch_pt2d<T, 2, 8, 2>(a, tmap, s);
     default: break;
   }
-  const int nchunk = (int)((a.g.S[1] + a.rows - 1) / a.rows);
+  KArgs<T> am = a;
+  if (am.rows <= 0) am.rows = auto_rows_2d(a.g);
+  const int nchunk = (int)((a.g.S[1] + am.rows - 1) / am.rows);
   const int ntask = a.g.nwin * nchunk;
   const int wpb = 4;
   const int grid = (ntask + wpb - 1) / wpb;
@@ -1280,9 +1285,9 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   if (v == 10) return launch_tile2d<T, 1, 16>(a, s);
   if (v == 11) return launch_tile2d<T, 1, 8>(a, s);
   if (v == 14) return launch_tile2d<T, 2, 8>(a, s);
-  if (v == 4) k_step2d<T, 4><<<grid, 32 * wpb, sm, s>>>(a, a.g.nwin, ntask);
-  else if (v == 2) k_step2d<T, 2><<<grid, 32 * wpb, sm, s>>>(a, a.g.nwin, ntask);
-  else k_step2d<T, 3><<<grid, 32 * wpb, sm, s>>>(a, a.g.nwin, ntask);
+  if (v == 4) k_step2d<T, 4><<<grid, 32 * wpb, sm, s>>>(am, a.g.nwin, ntask);
+  else if (v == 2) k_step2d<T, 2><<<grid, 32 * wpb, sm, s>>>(am, a.g.nwin, ntask);
+  else k_step2d<T, 3><<<grid, 32 * wpb, sm, s>>>(am, a.g.nwin, ntask);
 }
 
 template <typename T>

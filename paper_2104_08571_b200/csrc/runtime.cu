@@ -400,7 +400,8 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
     }
   }
   d->rows = c->rows_per_chunk;
-  if (d->rows <= 0) d->rows = g.D == 2 ? auto_rows_2d(g) : (g.D == 3 ? auto_rows_3d(g) : 1);
+  // 0 = each fused launcher picks its own chunking (2-D); 3-D z-chunk planes:
+  if (d->rows <= 0 && g.D == 3) d->rows = auto_rows_3d(g);
   if (c->nranks > 1) {
     if (!g_nccl.load()) return fail(RPL_E_NCCL, "libnccl.so.2 not found (set RPL_NCCL_LIB)");
     ncclUniqueId id;
