@@ -775,7 +775,7 @@ static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
 //   update warp j updates row k with faces k (own) and k+1 (warp j+1); the last
 //          warp's update waits for the next step's first face (read back from
 //          the rings), so every row is x-swept once and every face computed once.
-// TMA streams the step boxes [NW rows][C][W+AL] into an NS-stage ring, NS-1
+// TMA streams the step boxes [NW rows][C][W+AL] into an NS-stage ring, NS
 // steps ahead, continuously across the CTA's work items (persistent grid).
 // ---------------------------------------------------------------------------
 template <typename T, int V, int NW>
@@ -835,7 +835,8 @@ __global__ void __launch_bounds__(32 * NW, MB)
     fence_barrier_init();
   }
   __syncthreads();
-  // producer cursor (thread 0) runs NS-1 steps ahead of the consumers
+  // producer cursor (thread 0) runs NS steps ahead of the consumers: a stage is
+  // refilled right after barrier A of the step that consumed it
   CMCursor pc;
   int pseq = 0;
   auto issue_one = [&]() {
@@ -851,7 +852,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
   };
   if (threadIdx.x == 0) {
     pc.set(0, nwin, chunk, SY, NW, G, nwork);
-    for (int s = 0; s < SM::NS - 1; ++s) issue_one();
+    for (int s = 0; s < SM::NS; ++s) issue_one();
   }
   CMCursor cc;
   cc.set(0, nwin, chunk, SY, NW, G, nwork);

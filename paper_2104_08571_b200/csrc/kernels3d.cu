@@ -64,8 +64,8 @@ struct Smem3 {
   static constexpr size_t bytes() { return (size_t)(NS * STAGE + XY + FY) * sizeof(T) + 64; }
 };
 
-template <typename T, int V, int TY>
-__global__ void __launch_bounds__(32 * (TY + 2), 1)
+template <typename T, int V, int TY, int MB>
+__global__ void __launch_bounds__(32 * (TY + 2), MB)
     k_step3d(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
              int nwin, int nyb) {
   constexpr int D = 3, C = 5, W = 32 * V, R = TY + 2;
@@ -319,7 +319,7 @@ int make_tmap(const Geom& g, const void* buf, void* map_out, int box_w, int box_
 
 int window3d(const Geom& g) { return 30; }
 
-template <typename T, int V, int TY>
+template <typename T, int V, int TY, int MB = 1>
 static int launch3(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   constexpr int W = 32 * V;
   const Geom& g = a.g;
@@ -329,10 +329,11 @@ static int launch3(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   const size_t sm = Smem3<TY, V, T>::bytes();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_step3d<T, V, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_step3d<T, V, TY, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
     attr = true;
   }
-  k_step3d<T, V, TY><<<nwin * nyb * nzc, 32 * (TY + 2), sm, s>>>(
+  k_step3d<T, V, TY, MB><<<nwin * nyb * nzc, 32 * (TY + 2), sm, s>>>(
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb);
   return 0;
 }
@@ -343,6 +344,7 @@ int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 21: return launch3<T, 2, 14>(a, tmap, s);
     case 50: return launch3<T, 1, 30>(a, tmap, s);
     case 51: return launch3<T, 1, 22>(a, tmap, s);
+    case 52: return launch3<T, 1, 14, 2>(a, tmap, s);
     default: return launch3<T, 1, 14>(a, tmap, s);
   }
 }
