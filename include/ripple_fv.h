@@ -71,6 +71,16 @@ typedef enum { RPL_BC_TRANSMISSIVE = 0, RPL_BC_PERIODIC = 1, RPL_BC_REFLECTIVE =
  * identical results.  ndim == 1 always runs SPLIT (one sweep). */
 typedef enum { RPL_KERNEL_FUSED = 0, RPL_KERNEL_SPLIT = 1 } rpl_kernel;
 
+/* Halo transport between ranks (nranks > 1), the padding transfers of
+ * P:840-927 / P:1417-1419:
+ *  NCCL: pack kernel -> grouped ncclSend/ncclRecv -> unpack kernel (needs nccl_id);
+ *  P2P:  the step kernel stores every halo cell straight into the neighbour's
+ *        buffer over NVLink peer memory (CUDA IPC mappings), then a one-warp
+ *        flag kernel orders the step against the neighbours (system-scope
+ *        release/acquire); no pack, no copy, no NCCL.  Needs rpl_p2p_export /
+ *        rpl_p2p_attach after rpl_create and a library-owned arena. */
+typedef enum { RPL_TRANSPORT_NCCL = 0, RPL_TRANSPORT_P2P = 1 } rpl_transport;
+
 typedef struct {
   int32_t ndim;            /* 1, 2 or 3 */
   int64_t size[3];         /* global interior cells per dim, x fastest; unused dims 1 */
@@ -93,6 +103,7 @@ typedef struct {
   void* arena;             /* optional caller-owned device memory of rpl_arena_bytes() bytes */
   int32_t rows_per_chunk;  /* fused kernels: rows (2-D) / planes (3-D) marched per warp task;
                               0 -> automatic */
+  rpl_transport transport; /* nranks > 1: NCCL (default) or P2P */
 } rpl_config;
 
 /* Fill *cfg with defaults: ndim 1, size {1,1,1}, pad 2, parts {1,1,1}, F64, SOA,
@@ -186,6 +197,16 @@ typedef struct {
 } rpl_halo_edge;
 rpl_status rpl_halo_plan(const rpl_config* cfg, rpl_halo_edge* edges, int32_t max_edges,
                          int32_t* n_edges);
+
+/* P2P transport, step 1 (after rpl_create): write this rank's CUDA IPC handle
+ * blob (at most *blob_bytes bytes; *blob_bytes receives the size used, the same
+ * on every rank).  With blob == NULL only the size is returned. */
+rpl_status rpl_p2p_export(rpl_domain* dom, void* blob, size_t* blob_bytes);
+
+/* P2P transport, step 2 (collective): `blobs` = the blobs of all ranks in rank
+ * order (e.g. all_gather through the caller's process group), each blob_bytes
+ * long.  Maps every peer's buffers; halos then travel inside the step kernels. */
+rpl_status rpl_p2p_attach(rpl_domain* dom, const void* blobs, size_t blob_bytes);
 
 /* Free everything (collective). */
 void rpl_destroy(rpl_domain* dom);

@@ -18,6 +18,7 @@ STATUS = {0: "RPL_OK", -1: "RPL_E_INVALID_ARG", -2: "RPL_E_NOT_DIVISIBLE",
 F32, F64 = 0, 1
 SOA, AOS = 0, 1
 FUSED, SPLIT = 0, 1
+TRANSPORT_NCCL, TRANSPORT_P2P = 0, 1
 BC_TRANSMISSIVE, BC_PERIODIC, BC_REFLECTIVE = 0, 1, 2
 MAP_TRANSLATE, MAP_REFLECT, MAP_BROADCAST = 0, 1, 2
 
@@ -30,7 +31,7 @@ class Config(ctypes.Structure):
                 ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("nccl_id", ctypes.c_void_p), ("device", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("arena", ctypes.c_void_p),
-                ("rows_per_chunk", ctypes.c_int32)]
+                ("rows_per_chunk", ctypes.c_int32), ("transport", ctypes.c_int)]
 
 
 class HaloEdge(ctypes.Structure):
@@ -44,7 +45,7 @@ EXPORTS = ["rpl_config_init", "rpl_config_check", "rpl_arena_bytes", "rpl_nccl_u
            "rpl_create", "rpl_local_box", "rpl_set_state", "rpl_get_state", "rpl_get_padded",
            "rpl_fill_padding", "rpl_advance", "rpl_max_wavespeed", "rpl_advance_cfl",
            "rpl_synchronize", "rpl_launches_per_step", "rpl_profile", "rpl_profile_read",
-           "rpl_halo_plan", "rpl_destroy",
+           "rpl_halo_plan", "rpl_p2p_export", "rpl_p2p_attach", "rpl_destroy",
            "rpl_last_error"]
 
 _lib = None
@@ -81,6 +82,8 @@ def lib():
     L.rpl_profile.argtypes = [vp, ctypes.c_int32]
     L.rpl_profile_read.argtypes = [vp, P(ctypes.c_double), P(ctypes.c_int64)]
     L.rpl_halo_plan.argtypes = [P(Config), P(HaloEdge), ctypes.c_int32, P(ctypes.c_int32)]
+    L.rpl_p2p_export.argtypes = [vp, vp, P(ctypes.c_size_t)]
+    L.rpl_p2p_attach.argtypes = [vp, vp, ctypes.c_size_t]
     L.rpl_destroy.argtypes = [vp]
     L.rpl_destroy.restype = None
     L.rpl_last_error.argtypes = []

@@ -229,13 +229,23 @@ struct rpl_domain {
     unsigned char b[128];
   };
   TMap tmap[2][kMaxParts];
-  bool tmaps_ok = false;  // RPL_VARIANT env: fused-kernel occupancy variant (tuning)
+  bool tmaps_ok = false;
+  // P2P transport
+  unsigned long long* ctl = nullptr;        // [0,64): step flags from each rank, [64,128): max slots
+  int64_t base_off = 0;                     // arena -> 256-aligned buffer base
+  bool p2p = false, p2p_attached = false;
+  void* peer_arena[kMaxParts] = {nullptr};  // IPC mappings (to close)
+  unsigned long long** d_peer_ctl = nullptr;  // device [nranks]: each rank's control block
+  unsigned long long epoch = 0;  // RPL_VARIANT env: fused-kernel occupancy variant (tuning)
   // kernel timing (rpl_profile)
   std::vector<cudaEvent_t> ev;  // pairs
   size_t ev_used = 0;
 };
 
 static int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// control block after the buffers: P2P step flags [64] and wavespeed slots [64]
+constexpr int64_t kCtlBytes = 2 * kMaxParts * 8;
 
 extern "C" void rpl_config_init(rpl_config* c) {
   memset(c, 0, sizeof(*c));
@@ -270,7 +280,14 @@ static rpl_status geom_of(const rpl_config* c, Geom* g) {
   if (c->nranks > 1 && c->nranks != g->nparts)
     return fail(RPL_E_INVALID_ARG, "nranks must be 1 or prod(parts) (one partition per rank)");
   if (c->rank < 0 || c->rank >= c->nranks) return fail(RPL_E_INVALID_ARG, "rank out of range");
-  if (c->nranks > 1 && !c->nccl_id) return fail(RPL_E_INVALID_ARG, "nccl_id required");
+  if (c->transport != RPL_TRANSPORT_NCCL && c->transport != RPL_TRANSPORT_P2P)
+    return fail(RPL_E_INVALID_ARG, "transport");
+  if (c->nranks > 1 && c->transport == RPL_TRANSPORT_NCCL && !c->nccl_id)
+    return fail(RPL_E_INVALID_ARG, "nccl_id required");
+  if (c->nranks > 32 && c->transport == RPL_TRANSPORT_P2P)
+    return fail(RPL_E_INVALID_ARG, "P2P transport supports at most 32 ranks");
+  if (c->transport == RPL_TRANSPORT_P2P && c->nranks > 1 && c->arena)
+    return fail(RPL_E_INVALID_ARG, "P2P transport needs a library-owned arena (CUDA IPC)");
   if (c->rows_per_chunk < 0) return fail(RPL_E_INVALID_ARG, "rows_per_chunk must be >= 0");
   return RPL_OK;
 }
@@ -289,7 +306,7 @@ extern "C" rpl_status rpl_arena_bytes(const rpl_config* c, size_t* out) {
   rpl_status st = geom_of(c, &g);
   if (st) return st;
   const int nloc = c->nranks > 1 ? 1 : g.nparts;
-  *out = (size_t)(2 * nloc * part_bytes(g) + 256);
+  *out = (size_t)(2 * nloc * part_bytes(g) + kCtlBytes + 256);
   return RPL_OK;
 }
 
@@ -327,6 +344,9 @@ static void free_events(rpl_domain* d) {
 static void free_domain(rpl_domain* d) {
   if (!d) return;
   free_events(d);
+  for (int r = 0; r < kMaxParts; ++r)
+    if (d->peer_arena[r]) cudaIpcCloseMemHandle(d->peer_arena[r]);
+  if (d->d_peer_ctl) cudaFree(d->d_peer_ctl);
   if (d->comm) g_nccl.CommDestroy(d->comm);
   if (d->own_arena && d->arena) cudaFree(d->arena);
   if (d->d_tab) cudaFree(d->d_tab);
@@ -371,7 +391,9 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
   const int64_t pb = part_bytes(g);
   for (size_t i = 0; i < d->local.size(); ++i)
     for (int b = 0; b < 2; ++b) d->buf[b][d->local[i]] = base + (2 * i + b) * pb;
-  CU(cudaMemsetAsync(base, 0, 2 * d->local.size() * pb, d->stream));
+  CU(cudaMemsetAsync(base, 0, 2 * d->local.size() * pb + kCtlBytes, d->stream));
+  d->ctl = reinterpret_cast<unsigned long long*>(base + 2 * d->local.size() * pb);
+  d->base_off = base - (char*)d->arena;
   CU(cudaMalloc(&d->d_tab, sizeof(void*) * 2 * kMaxParts));
   CU(cudaMemcpy(d->d_tab, d->buf, sizeof(void*) * 2 * kMaxParts, cudaMemcpyHostToDevice));
   CU(cudaMalloc(&d->d_flag, sizeof(unsigned)));
@@ -402,7 +424,9 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
   d->rows = c->rows_per_chunk;
   // 0 = each fused launcher picks its own chunking (2-D); 3-D z-chunk planes:
   if (d->rows <= 0 && g.D == 3) d->rows = auto_rows_3d(g);
-  if (c->nranks > 1) {
+  d->p2p = c->nranks > 1 && c->transport == RPL_TRANSPORT_P2P;
+  if (d->p2p) CU(cudaMalloc(&d->d_peer_ctl, sizeof(void*) * kMaxParts));
+  if (c->nranks > 1 && !d->p2p) {
     if (!g_nccl.load()) return fail(RPL_E_NCCL, "libnccl.so.2 not found (set RPL_NCCL_LIB)");
     ncclUniqueId id;
     memcpy(&id, c->nccl_id, sizeof(id));
@@ -636,16 +660,69 @@ static rpl_status exchange_t(rpl_domain* d, int b) {
   return RPL_OK;
 }
 
+// P2P: one warp publishes "rank `me` finished epoch e" into every peer's control
+// block (system-scope release after a system fence, so the step kernel's peer
+// stores are visible first) and waits until every peer published e (acquire).
+// With mode 1 it also publishes the local wavespeed max into the peers' slots
+// and reduces the slots afterwards (exact: max).
+__global__ void k_p2p_sync(unsigned long long* const* ctl, int me, int nranks,
+                           unsigned long long epoch, unsigned long long* smax, int mode) {
+  const int r = threadIdx.x;
+  unsigned long long* mine = ctl[me];
+  if (r < nranks && r != me) {
+    unsigned long long* peer = ctl[r];
+    if (mode == 1) {
+      const unsigned long long v = *smax;
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(peer + kMaxParts + me), "l"(v)
+                   : "memory");
+    }
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer + me), "l"(epoch) : "memory");
+    unsigned long long got = 0;
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(got) : "l"(mine + r) : "memory");
+      if (got < epoch) __nanosleep(64);
+    } while (got < epoch);
+  }
+  __syncwarp();
+  if (mode == 1 && r == 0) {
+    unsigned long long m = *smax;
+    for (int q = 0; q < nranks; ++q)
+      if (q != me) {
+        unsigned long long v;
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + kMaxParts + q)
+                     : "memory");
+        m = v > m ? v : m;
+      }
+    *smax = m;
+  }
+}
+
+static rpl_status p2p_sync(rpl_domain* d, int mode) {
+  if (!d->p2p_attached) return fail(RPL_E_INVALID_ARG, "P2P transport: call rpl_p2p_attach first");
+  ++d->epoch;
+  k_p2p_sync<<<1, 32, 0, d->stream>>>(d->d_peer_ctl, d->cfg.rank, d->cfg.nranks, d->epoch,
+                                      d->d_smax, mode);
+  CU(cudaGetLastError());
+  return RPL_OK;
+}
+
 static rpl_status exchange(rpl_domain* d, int b) {
   if (d->cfg.nranks <= 1) return RPL_OK;
+  if (d->p2p) return p2p_sync(d, 0);  // halos were stored by the step kernel itself
   return d->g.elem == 8 ? exchange_t<double>(d, b) : exchange_t<float>(d, b);
 }
 
 template <typename T>
 static rpl_status fill_t(rpl_domain* d) {
+  if (d->p2p) {  // peers' states must be set before k_fill reads their interiors
+    rpl_status st = p2p_sync(d, 0);
+    if (st) return st;
+  }
   T* const* tab = (T* const*)(d->d_tab + d->cur * kMaxParts);
   for (int p : d->local) launch_fill<T>(d->g, p, tab, d->stream);
   CU(cudaGetLastError());
+  if (d->p2p) return RPL_OK;  // k_fill read the peers' interiors directly
   return exchange(d, d->cur);
 }
 
@@ -670,6 +747,7 @@ extern "C" rpl_status rpl_launches_per_step(const rpl_domain* d, int32_t* out) {
   for (auto& P : d->send_peers) ne += (int)P.edges.size();
   for (auto& P : d->recv_peers) ne += (int)P.edges.size();
   n += ne * (use_fused(d) ? 1 : d->g.D);
+  if (d->p2p) n += use_fused(d) ? 1 : d->g.D;  // one flag kernel per exchange
   *out = n;
   return RPL_OK;
 }
@@ -744,8 +822,12 @@ extern "C" rpl_status rpl_max_wavespeed(rpl_domain* d, double* out) {
                           d->d_flag, d->stream);
   }
   CU(cudaGetLastError());
-  if (d->cfg.nranks > 1)
+  if (d->cfg.nranks > 1 && d->p2p) {
+    rpl_status st = p2p_sync(d, 1);
+    if (st) return st;
+  } else if (d->cfg.nranks > 1) {
     NC(g_nccl.AllReduce(d->d_smax, d->d_smax, 1, ncclUint64, ncclMax, d->comm, d->stream));
+  }
   CU(cudaMemcpyAsync(d->h_smax, d->d_smax, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                      d->stream));
   rpl_status st = check_flag(d);
@@ -822,5 +904,68 @@ extern "C" rpl_status rpl_profile_read(rpl_domain* d, double* kernel_ms, int64_t
   *kernel_ms = tot;
   *launches = (int64_t)(d->ev_used / 2);
   d->ev_used = 0;
+  return RPL_OK;
+}
+
+namespace {
+struct P2PBlob {
+  cudaIpcMemHandle_t h;
+  int64_t base_off;  // arena -> buffer base
+  int64_t pb;        // bytes per buffer
+  int64_t ctl_off;   // buffer base -> control block
+  int32_t rank, device;
+};
+}  // namespace
+
+extern "C" rpl_status rpl_p2p_export(rpl_domain* d, void* blob, size_t* blob_bytes) {
+  if (!d || !blob_bytes) return fail(RPL_E_INVALID_ARG, "null argument");
+  if (!d->p2p) return fail(RPL_E_INVALID_ARG, "domain was not created with RPL_TRANSPORT_P2P");
+  if (!blob) {
+    *blob_bytes = sizeof(P2PBlob);
+    return RPL_OK;
+  }
+  if (*blob_bytes < sizeof(P2PBlob)) return fail(RPL_E_INVALID_ARG, "blob too small");
+  CU(cudaSetDevice(d->device));
+  P2PBlob b;
+  memset(&b, 0, sizeof(b));
+  CU(cudaIpcGetMemHandle(&b.h, d->arena));
+  b.base_off = d->base_off;
+  b.pb = part_bytes(d->g);
+  b.ctl_off = 2 * b.pb;  // one local partition per rank
+  b.rank = d->cfg.rank;
+  b.device = d->device;
+  memcpy(blob, &b, sizeof(b));
+  *blob_bytes = sizeof(b);
+  return RPL_OK;
+}
+
+extern "C" rpl_status rpl_p2p_attach(rpl_domain* d, const void* blobs, size_t blob_bytes) {
+  if (!d || !blobs) return fail(RPL_E_INVALID_ARG, "null argument");
+  if (!d->p2p) return fail(RPL_E_INVALID_ARG, "domain was not created with RPL_TRANSPORT_P2P");
+  if (blob_bytes != sizeof(P2PBlob)) return fail(RPL_E_SHAPE_MISMATCH, "blob size mismatch");
+  CU(cudaSetDevice(d->device));
+  const int me = d->cfg.rank, n = d->cfg.nranks;
+  unsigned long long* ctl[kMaxParts] = {nullptr};
+  for (int r = 0; r < n; ++r) {
+    P2PBlob b;
+    memcpy(&b, (const char*)blobs + (size_t)r * blob_bytes, sizeof(b));
+    if (b.rank != r) return fail(RPL_E_INVALID_ARG, "blobs must be in rank order");
+    if (r == me) {
+      ctl[r] = d->ctl;
+      continue;
+    }
+    void* p = nullptr;
+    if (!d->peer_arena[r]) {
+      CU(cudaIpcOpenMemHandle(&p, b.h, cudaIpcMemLazyEnablePeerAccess));
+      d->peer_arena[r] = p;
+    }
+    char* base = (char*)d->peer_arena[r] + b.base_off;
+    d->buf[0][r] = base;
+    d->buf[1][r] = base + b.pb;
+    ctl[r] = reinterpret_cast<unsigned long long*>(base + b.ctl_off);
+  }
+  CU(cudaMemcpy(d->d_tab, d->buf, sizeof(void*) * 2 * kMaxParts, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d->d_peer_ctl, ctl, sizeof(void*) * kMaxParts, cudaMemcpyHostToDevice));
+  d->p2p_attached = true;
   return RPL_OK;
 }

@@ -30,7 +30,7 @@ def _bc(v):
 
 def make_config(size, pad=2, parts=None, dtype="f64", layout="soa", kernel="fused", gamma=1.4,
                 dx=None, bc_lo=None, bc_hi=None, nranks=1, rank=0, nccl_id=None, device=0,
-                stream=None, arena=None, rows_per_chunk=0):
+                stream=None, arena=None, rows_per_chunk=0, transport="nccl"):
     size = [int(v) for v in size]
     D = len(size)
     if not 1 <= D <= 3:
@@ -57,6 +57,7 @@ def make_config(size, pad=2, parts=None, dtype="f64", layout="soa", kernel="fuse
     cfg.stream = int(stream) if stream else None
     cfg.arena = int(arena) if arena else None
     cfg.rows_per_chunk = int(rows_per_chunk)
+    cfg.transport = {"nccl": N.TRANSPORT_NCCL, "p2p": N.TRANSPORT_P2P}[transport]
     return cfg
 
 
@@ -185,6 +186,21 @@ class Domain:
 
     def synchronize(self):
         N.check(N.lib().rpl_synchronize(self._h))
+
+    # -- P2P transport (nranks > 1): export IPC blob, all-gather it, attach
+    def p2p_export(self) -> bytes:
+        n = ctypes.c_size_t(0)
+        N.check(N.lib().rpl_p2p_export(self._h, None, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        N.check(N.lib().rpl_p2p_export(self._h, buf, ctypes.byref(n)))
+        return buf.raw[: n.value]
+
+    def p2p_attach(self, blobs):
+        """blobs: list of every rank's export blob, in rank order."""
+        size = len(blobs[0])
+        assert all(len(b) == size for b in blobs)
+        joined = b"".join(blobs)
+        N.check(N.lib().rpl_p2p_attach(self._h, joined, size))
 
     def profile(self, max_launches: int):
         """Record CUDA events around every step-kernel launch (0 disables)."""

@@ -1,0 +1,97 @@
+"""Multi-rank path on one GPU: 2-4 processes (one partition each) share cuda:0 and
+exchange halos through the P2P transport (CUDA IPC peer mappings written directly
+by the step kernels + system-scope flag kernel), with a gloo process group only
+for the IPC-handle all-gather.  Result must be bitwise equal to the single-rank
+run (BASELINE.json north_star: bit-identical across GPU counts)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, n, parts, kw, steps, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_08571_b200 as R
+    import workloads as W
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        D = len(n)
+        dx = [1.0 / n[0]] * D
+        dom = R.Domain(n, parts=parts, nranks=world, rank=rank, transport="p2p", dx=dx, **kw)
+        blob = dom.p2p_export()
+        blobs = [None] * world
+        dist.all_gather_object(blobs, blob)
+        dom.p2p_attach(blobs)
+        U = W.shock_bubble(n, dx=dx, box=(dom.lo, dom.hi))
+        if kw.get("dtype") == "f32":
+            U = U.astype(np.float32)
+        dom.set_state(U)
+        s = dom.max_wavespeed()
+        dom.advance(0.4 * dx[0] / s, steps)
+        out = dom.get_state()
+        q.put((rank, dom.lo, dom.hi, out, s))
+        dom.close()
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def _single(n, kw, steps):
+    import paper_2104_08571_b200 as R
+    import workloads as W
+    D = len(n)
+    dx = [1.0 / n[0]] * D
+    U = W.shock_bubble(n, dx=dx)
+    if kw.get("dtype") == "f32":
+        U = U.astype(np.float32)
+    with R.Domain(n, dx=dx, **kw) as dom:
+        dom.set_state(U)
+        s = dom.max_wavespeed()
+        dom.advance(0.4 * dx[0] / s, steps)
+        return dom.get_state(), s
+
+
+@pytest.mark.parametrize("n,parts,kw", [
+    ((130, 64), (1, 2), {}),
+    ((128, 96), (2, 1), dict(bc_lo=["periodic", "reflective"], bc_hi=["periodic", "clamp"])),
+    ((40, 32, 24), (1, 1, 2), dict(dtype="f32")),
+    ((40, 32, 24), (2, 2, 1), {}),
+])
+def test_p2p_ranks_bitwise_equal_single_rank(n, parts, kw):
+    world = int(np.prod(parts))
+    steps = 6
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_rank, args=(r, world, port, n, parts, kw, steps, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    ref, s_ref = _single(n, kw, steps)
+    D = len(n)
+    for rank, lo, hi, out, s in res:
+        assert s == s_ref
+        sl = tuple(slice(lo[d], hi[d]) for d in reversed(range(D)))
+        assert np.array_equal(out, ref[sl]), rank
