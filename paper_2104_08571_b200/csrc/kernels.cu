@@ -1096,8 +1096,10 @@ static void launch_cm2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, (int)chunk, nwork);
 }
 
-// 2-D fused variants (RPL_VARIANT): 0/32 persistent TMA V=1 NW=8 (default,
-// fastest measured), 30 V=1 NW=16, 31 V=2 NW=8, 33 V=2 NW=16;
+// 2-D fused variants (RPL_VARIANT): 0/34 persistent TMA V=1 NW=8, 3 CTAs/SM
+// (default, fastest measured: 29.2 us at 1024^2 fp64), 32 same at 2 CTAs/SM,
+// 30 V=1 NW=16, 31 V=2 NW=8, 33 V=2 NW=16, 35/36 other occupancies;
+// 40-43 column-march (correct, slower: 39-48 us);
 // 10/11/14 non-persistent tiles;
 // 2/3/4 per-warp march.  Box of the TMA variants:
 int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
@@ -1262,9 +1264,9 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   switch (a.variant) {
     case 30: return launch_pt2d<T, 1, 16>(a, tmap, s);
     case 31: return launch_pt2d<T, 2, 8>(a, tmap, s);
-    case 0: case 32: return launch_pt2d<T, 1, 8>(a, tmap, s);
+    case 32: return launch_pt2d<T, 1, 8>(a, tmap, s);
     case 33: return launch_pt2d<T, 2, 16>(a, tmap, s);
-    case 34: return launch_pt2d<T, 1, 8, 3>(a, tmap, s);
+    case 0: case 34: return launch_pt2d<T, 1, 8, 3>(a, tmap, s);
     case 40: return launch_cm2d<T, 1, 8, 3>(a, tmap, s);
     case 41: return launch_cm2d<T, 1, 8, 2>(a, tmap, s);
     case 42: return launch_cm2d<T, 2, 8, 2>(a, tmap, s);
