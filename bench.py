@@ -210,13 +210,23 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="2d1024", choices=sorted(WORKLOADS))
     ap.add_argument("--kernel", default="fused", choices=["fused", "split"])
+    ap.add_argument("--dtype", default=None, choices=["f32", "f64"],
+                    help="override the workload's dtype (configs[4] runs both)")
+    ap.add_argument("--layout", default="soa", choices=["soa", "aos"],
+                    help="HBM layout of the conserved-state struct (BASELINE configs[4])")
     ap.add_argument("--rows", type=int, default=0, help="rows per warp task (0 = auto)")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="halo transport between ranks (N > 1): P2P = step kernels store halos "
+                         "into the neighbour's buffer over NVLink (CUDA IPC); NCCL = pack + "
+                         "ncclSend/Recv + unpack")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.dtype:
+        wl["dtype"] = args.dtype
     if args.impl == "reference":
         return run_reference(args, wl)
 
@@ -244,15 +254,21 @@ def main():
     D = wl["ndim"]
     dx = [1.0 / wl["n"][0]] * D
     nccl_id = None
-    if world > 1:
+    if world > 1 and args.transport == "nccl":
         idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
             idt.copy_(torch.frombuffer(bytearray(R.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().numpy().tobytes())
     dom = R.Domain(gn, pad=2, parts=parts, dtype=wl["dtype"], kernel=args.kernel, dx=dx,
+                   layout=args.layout,
                    nranks=world, rank=rank if world > 1 else 0, nccl_id=nccl_id, device=dev,
-                   stream=stream.cuda_stream, rows_per_chunk=args.rows)
+                   stream=stream.cuda_stream, rows_per_chunk=args.rows,
+                   transport=args.transport if world > 1 else "nccl")
+    if world > 1 and args.transport == "p2p":
+        blobs = [None] * world
+        dist.all_gather_object(blobs, dom.p2p_export())
+        dom.p2p_attach(blobs)
     box = (dom.lo, dom.hi)
     U0 = W.shock_bubble(tuple(gn), dx=dx, box=box)
     if wl["dtype"] == "f32":
@@ -367,7 +383,8 @@ def main():
             "scaling": wl["scaling"], "vs_baseline": None, "dtype": wl["dtype"],
             "data": "synthetic",
             "config": {"workload": wl["label"], "global_cells": gn, "parts": parts,
-                       "kernel": args.kernel, "layout": "soa",
+                       "kernel": args.kernel, "layout": args.layout,
+                       "transport": args.transport if world > 1 else None,
                        "l2": "flushed between steps (256 MiB write), per-step CUDA events"
                              if flush is not None else "not flushed",
                        "timing": "sum of per-step CUDA events on the library stream, max over ranks",

@@ -64,7 +64,7 @@ struct Smem3 {
   static constexpr size_t bytes() { return (size_t)(NS * STAGE + XY + FY) * sizeof(T) + 64; }
 };
 
-template <typename T, int V, int TY, int MB>
+template <typename T, int V, int TY, int MB, int L>
 __global__ void __launch_bounds__(32 * (TY + 2), MB)
     k_step3d(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
              int nwin, int nyb) {
@@ -117,7 +117,8 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
     if (kz >= nplanes) return;
     const int s = kz % SM::NS;
     mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
-    tma_load_4d(stage + s * SM::STAGE, &tmap, &bar[s], tx, 0, ty, (int)(g.off[2] + z0 - 1 + kz));
+    tma_load_4d(stage + s * SM::STAGE, &tmap, &bar[s], L == 0 ? tx : tx * C, 0, ty,
+                (int)(g.off[2] + z0 - 1 + kz));
   };
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
   ZState<T, V> zs;
   int bad = 0, nan = 0;
   const T qx = a.q[0], nqx = a.nq2[0], qy = a.q[1], nqy = a.nq2[1], qz = a.q[2], nqz = a.nq2[2];
-  T* dst_row = a.out + g.row(yr, z0 - 1) * g.rstride + g.xo + xw + V * lane;
+  T* dst_row = a.out + g.row(yr, z0 - 1) * g.rstride + (g.xo + xw + V * lane) * g.xstride;
   const int64_t plane = g.rstride * g.P[1];
 
   for (int kz = 0; kz < nplanes; ++kz) {
@@ -136,11 +137,13 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
     mbar_wait(&bar[s], (kz / SM::NS) & 1);
     // ---------------- X: this warp's row
     T U[V][C], F[V][C], S_[V][C], G[V][C];
-    const T* st = stage + s * SM::STAGE + warp * C * SM::WB + sh + V * lane;
+    // stage row layout: SoA box [C][WB] (x fastest), AoS box [WB][C] (component fastest)
+    const T* st = stage + s * SM::STAGE + warp * C * SM::WB +
+                  (L == 0 ? sh + V * lane : (sh + V * lane) * C);
 #pragma unroll
     for (int c = 0; c < C; ++c)
 #pragma unroll
-      for (int v = 0; v < V; ++v) U[v][c] = st[c * SM::WB + v];
+      for (int v = 0; v < V; ++v) U[v][c] = L == 0 ? st[c * SM::WB + v] : st[v * C + c];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int b = phys_flux<D, 0>(U[v], F[v], gm1);
@@ -235,13 +238,13 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
             if (out_ok[v] & row_out) {
               nan = max(nan, max(naninf(o[v][0]), naninf(o[v][C - 1])));
 #pragma unroll
-              for (int c = 0; c < C; ++c) dp[c * g.cstride + v] = o[v][c];
+              for (int c = 0; c < C; ++c) dp[c * g.cstride + v * g.xstride] = o[v][c];
               const bool zf = (z - 1 < g.pad) | (z - 1 >= SZ - g.pad);
               if (xface[v] | yface | zf) {
                 if (g.img_fast)
                   images_single<D>(g, a.out, xs[v], yr, z - 1, o[v]);
                 else
-                  images3_nl<D, 0, T>(&a, xs[v], yr, z - 1, o[v][0], o[v][1], o[v][2], o[v][3],
+                  images3_nl<D, L, T>(&a, xs[v], yr, z - 1, o[v][0], o[v][1], o[v][2], o[v][3],
                                       o[v][4]);
               }
             }
@@ -319,7 +322,7 @@ int make_tmap(const Geom& g, const void* buf, void* map_out, int box_w, int box_
 
 int window3d(const Geom& g) { return 30; }
 
-template <typename T, int V, int TY, int MB = 1>
+template <typename T, int V, int TY, int MB = 1, int L = 0>
 static int launch3(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   constexpr int W = 32 * V;
   const Geom& g = a.g;
@@ -329,17 +332,18 @@ static int launch3(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   const size_t sm = Smem3<TY, V, T>::bytes();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_step3d<T, V, TY, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_step3d<T, V, TY, MB, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
     attr = true;
   }
-  k_step3d<T, V, TY, MB><<<nwin * nyb * nzc, 32 * (TY + 2), sm, s>>>(
+  k_step3d<T, V, TY, MB, L><<<nwin * nyb * nzc, 32 * (TY + 2), sm, s>>>(
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb);
   return 0;
 }
 
 template <typename T>
 int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  if (a.g.layout == 1) return launch3<T, 1, 14, 1, 1>(a, tmap, s);  // AoS (configs[4])
   switch (a.variant) {
     case 21: return launch3<T, 2, 14>(a, tmap, s);
     case 50: return launch3<T, 1, 30>(a, tmap, s);
@@ -349,7 +353,26 @@ int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   }
 }
 
+// AoS: the (x, component) pair is one contiguous dimension of pitch*C elements
+int make_tmap_aos(const Geom& g, const void* buf, void* map_out, int box_cells, int box_rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return -1;
+  const cuuint64_t dims[4] = {(cuuint64_t)(g.pitch * g.C), 1, (cuuint64_t)g.P[1],
+                              (cuuint64_t)g.P[2]};
+  const cuuint64_t strides[3] = {(cuuint64_t)(g.rstride * g.elem), (cuuint64_t)(g.rstride * g.elem),
+                                 (cuuint64_t)(g.rstride * g.P[1] * g.elem)};
+  const cuuint32_t box[4] = {(cuuint32_t)(box_cells * g.C), 1, (cuuint32_t)box_rows, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(map_out),
+                   g.elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                   4, const_cast<void*>(buf), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 int make_tmap3d(const Geom& g, const void* buf, void* map_out, int variant) {
+  if (g.layout == 1) return make_tmap_aos(g, buf, map_out, 32 + 16 / g.elem, 14 + 2);
   return make_tmap(g, buf, map_out, win3(g, variant) + 16 / g.elem,  // + Smem3::AL
                    ty3(variant) + 2);
 }

@@ -402,7 +402,7 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
   CU(cudaMallocHost(&d->h_flag, sizeof(unsigned)));
   CU(cudaMallocHost(&d->h_smax, sizeof(unsigned long long)));
   if (const char* v = getenv("RPL_VARIANT")) d->variant = atoi(v);
-  if (g.D == 3 && g.layout == 0) {
+  if (g.D == 3) {  // SoA and AoS
     d->tmaps_ok = true;
     for (int p : d->local)
       for (int b = 0; b < 2; ++b) {
@@ -736,8 +736,8 @@ extern "C" rpl_status rpl_fill_padding(rpl_domain* d) {
 }
 
 static bool use_fused(const rpl_domain* d) {
-  return d->cfg.kernel == RPL_KERNEL_FUSED && d->g.layout == 0 &&
-         (d->g.D == 2 || (d->g.D == 3 && d->tmaps_ok));
+  return d->cfg.kernel == RPL_KERNEL_FUSED &&
+         ((d->g.D == 2 && d->g.layout == 0) || (d->g.D == 3 && d->tmaps_ok));
 }
 
 extern "C" rpl_status rpl_launches_per_step(const rpl_domain* d, int32_t* out) {
