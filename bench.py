@@ -240,9 +240,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # RPL_SHARE_DEVICE=1: every rank on cuda:0 (functional check of the N>1 path on
+    # a 1-GPU box; timings are then meaningless: the processes time-slice one GPU)
+    share = os.environ.get("RPL_SHARE_DEVICE") == "1"
+    backend = "nccl" if args.transport == "nccl" else "gloo"  # P2P: host coordination only
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        torch.cuda.set_device(0 if share else local_rank)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
@@ -324,7 +331,8 @@ def main():
     dom.profile(0)
     t_total = sum(step_ms) / 1e3
     if world > 1:
-        tt = torch.tensor([t_total], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([t_total], dtype=torch.float64,
+                          device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_total = float(tt.item())
     dom.synchronize()  # surfaces any domain error of the timed steps
@@ -351,7 +359,8 @@ def main():
         torch.cuda.synchronize()
         te = e0.elapsed_time(e1) / 1e3
         if world > 1:
-            tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+            tt = torch.tensor([te], dtype=torch.float64,
+                              device="cuda" if backend == "nccl" else "cpu")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
         nb = C * local_cells * elem
