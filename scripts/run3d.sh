@@ -1,0 +1,17 @@
+#!/bin/bash
+TAG=${1:-run3d}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+timeout 900 python -m pytest tests -m gpu -q -x > $OUT/pytest_gpu.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu.log
+for w in s512 w384 l256; do
+  timeout 300 python bench.py --workload $w --steps 10 --no-cpu-baseline --e2e-steps 0 > $OUT/b_${w}.json 2>>$OUT/err.log
+done
+OUT=$OUT python - <<'PY' > $OUT/summary.txt
+import json,glob,os
+for f in sorted(glob.glob(os.environ['OUT']+'/b_*.json')):
+    try:
+        d=json.loads(open(f).read().strip().splitlines()[-1]); r=d['roofline']
+        print(f"{os.path.basename(f):28s} {d['value']:7.2f} Gcell/s {r['kernel']:9s} {r['launch_ms']*1e3:9.1f} us/launch frac {r['frac']:.3f}")
+    except Exception as e: print(f, 'ERR', e)
+PY
+cat $OUT/summary.txt; tail -3 $OUT/pytest_gpu.log
