@@ -22,6 +22,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "async.cuh"
 #include "kernels.hpp"
@@ -281,6 +282,19 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+// L2 sector promotion of the TMA loads (RPL_L2PROMO: 0 none, 1 64B, 2 128B, 3 256B;
+// default 2 -- the SoA box rows are only 136-272 bytes long)
+static CUtensorMapL2promotion l2_promotion() {
+  int v = 2;
+  if (const char* e = getenv("RPL_L2PROMO")) v = atoi(e);
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 3: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  }
+}
+
 static EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
@@ -324,7 +338,7 @@ int make_tmap(const Geom& g, const void* buf, void* map_out, int box_w, int box_
                    g.elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                    4, const_cast<void*>(buf), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
@@ -375,7 +389,7 @@ int make_tmap_aos(const Geom& g, const void* buf, void* map_out, int box_cells, 
                    g.elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                    4, const_cast<void*>(buf), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
