@@ -126,14 +126,13 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
     for (int s = 0; s < SM::NS; ++s) issue(s);
   }
 
+  ZState<T, V> zs;
   int bad = 0, nan = 0;
   const T qx = a.q[0], nqx = a.nq2[0], qy = a.q[1], nqy = a.nq2[1], qz = a.q[2], nqz = a.nq2[2];
   T* dst_row = a.out + g.row(yr, z0 - 1) * g.rstride + (g.xo + xw + V * lane) * g.xstride;
   const int64_t plane = g.rstride * g.P[1];
 
-  // the z-march state ping-pongs between two register sets (loop unrolled by
-  // two planes), so no per-plane state copies are needed
-  auto plane_step = [&](const int kz, const ZState<T, V>& zin, ZState<T, V>& zout) {
+  for (int kz = 0; kz < nplanes; ++kz) {
     const int z = z0 - 1 + kz;
     const int s = kz % SM::NS;
     mbar_wait(&bar[s], (kz / SM::NS) & 1);
@@ -226,14 +225,14 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
         T Pz[V][C];
 #pragma unroll
         for (int v = 0; v < V; ++v)
-          force_face<D, 2>(zin.us[v], zin.fz[v], Us[v], Gz[v], Pz[v], qz, nqz, gm1);
+          force_face<D, 2>(zs.us[v], zs.fz[v], Us[v], Gz[v], Pz[v], qz, nqz, gm1);
         if (kz >= 2) {
           // update and store plane z-1
           T o[V][C];
 #pragma unroll
           for (int v = 0; v < V; ++v)
 #pragma unroll
-            for (int c = 0; c < C; ++c) o[v][c] = zin.us[v][c] - (Pz[v][c] - zin.ph[v][c]);
+            for (int c = 0; c < C; ++c) o[v][c] = zs.us[v][c] - (Pz[v][c] - zs.ph[v][c]);
           T* dp = dst_row + (int64_t)(kz - 1) * plane;
 #pragma unroll
           for (int v = 0; v < V; ++v) {
@@ -255,24 +254,17 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
 #pragma unroll
         for (int v = 0; v < V; ++v)
 #pragma unroll
-          for (int c = 0; c < C; ++c) zout.ph[v][c] = Pz[v][c];
+          for (int c = 0; c < C; ++c) zs.ph[v][c] = Pz[v][c];
       }
 #pragma unroll
       for (int v = 0; v < V; ++v)
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          zout.us[v][c] = Us[v][c];
-          zout.fz[v][c] = Gz[v][c];
+          zs.us[v][c] = Us[v][c];
+          zs.fz[v][c] = Gz[v][c];
         }
     }
-    };
-  ZState<T, V> zA, zB;
-  int kz = 0;
-  for (; kz + 1 < nplanes; kz += 2) {
-    plane_step(kz, zA, zB);
-    plane_step(kz + 1, zB, zA);
   }
-  if (kz < nplanes) plane_step(kz, zA, zB);
   if (__any_sync(0xffffffffu, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
 }
 
