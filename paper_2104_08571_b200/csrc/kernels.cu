@@ -1096,6 +1096,297 @@ static void launch_cm2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, (int)chunk, nwork);
 }
 
+// ---------------------------------------------------------------------------
+// K-B (2-D), point-to-point form: the tile work of k_step2d_pt without CTA-wide
+// barriers.  A producer warp issues the TMA boxes (full/empty mbarrier ring);
+// compute warp j only waits for the rows it actually needs -- row j-1's
+// (U*, F_y) (xyReady), the face computed by warp j+1 (fyReady) -- and signals
+// when it is done reading a neighbour's slot (xyFree / fyFree), so warps drift
+// across tiles instead of meeting at __syncthreads (the publish buffers are
+// double-buffered by tile parity).
+// ---------------------------------------------------------------------------
+template <typename T, int V, int NW>
+struct SmemPP {
+  static constexpr int W = 32 * V, C = 4, NS = 3;
+  static constexpr int AL = 16 / (int)sizeof(T);
+  static constexpr int WB = W + AL;
+  static constexpr int STAGE = NW * C * WB;
+  static constexpr int XY = 2 * NW * 2 * C * W;
+  static constexpr int FY = 2 * (NW - 1) * C * W;
+  static constexpr int NBAR = 2 * NS + 2 * NW + 2 * (NW - 1) + 2 * NW + 2 * (NW - 1);
+  static constexpr size_t bytes() {
+    return (size_t)(NS * STAGE + XY + FY) * sizeof(T) + NBAR * 8 + 64;
+  }
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <typename T, int V, int NW, int MB>
+__global__ void __launch_bounds__(32 * (NW + 1), MB)
+    k_step2d_pp(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
+                int nwin, int ntiles) {
+  constexpr int D = 2, C = 4, W = 32 * V;
+  using SM = SmemPP<T, V, NW>;
+  using VT = typename VecV<T, V>::type;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  T* stage = reinterpret_cast<T*>(smem);
+  T* xy = stage + SM::NS * SM::STAGE;  // [2][NW][2C][W]
+  T* fy = xy + SM::XY;                 // [2][NW-1][C][W]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(fy + SM::FY);
+  uint64_t* full = bars;                       // [NS]
+  uint64_t* empty = full + SM::NS;             // [NS]
+  uint64_t* xyReady = empty + SM::NS;          // [2][NW]
+  uint64_t* fyReady = xyReady + 2 * NW;        // [2][NW-1]
+  uint64_t* xyFree = fyReady + 2 * (NW - 1);   // [2][NW]
+  uint64_t* fyFree = xyFree + 2 * NW;          // [2][NW-1]
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int SX = (int)g.S[0], SY = (int)g.S[1];
+  const int G = gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < SM::NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NW);
+    }
+    for (int i = 0; i < 2 * NW; ++i) {
+      mbar_init(&xyReady[i], 1);
+      mbar_init(&xyFree[i], 1);
+    }
+    for (int i = 0; i < 2 * (NW - 1); ++i) {
+      mbar_init(&fyReady[i], 1);
+      mbar_init(&fyFree[i], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == NW) {  // ---------------- producer warp
+    if (lane == 0) {
+      for (int it = 0;; ++it) {
+        const int tile = blockIdx.x + it * G;
+        if (tile >= ntiles) break;
+        const int s = it % SM::NS;
+        if (it >= SM::NS) mbar_wait(&empty[s], ((it / SM::NS) - 1) & 1);
+        const int w = tile % nwin, yb = tile / nwin;
+        const int x0 = (int)g.xo + w * (W - 2) - 1;
+        mbar_arrive_expect_tx(&full[s], SM::STAGE * (unsigned)sizeof(T));
+        tma_load_box(stage + s * SM::STAGE, &tmap, &full[s], x0 - x0 % SM::AL, 0,
+                     (int)g.off[1] + yb * (NW - 2) - 1, 0);
+      }
+    }
+    return;
+  }
+  // ---------------- compute warps
+  const T gm1 = a.gm1, qx = a.q[0], nqx = a.nq2[0], qy = a.q[1], nqy = a.nq2[1];
+  int bad = 0, nan = 0;
+  for (int it = 0;; ++it) {
+    const int tile = blockIdx.x + it * G;
+    if (tile >= ntiles) break;
+    const int p = it & 1, u = it >> 1;
+    const int win = tile % nwin, yb = tile / nwin;
+    const int xw = win * (W - 2) - 1;
+    const int yr = yb * (NW - 2) - 1 + warp;
+    const bool row_in = yr <= SY;
+    const int s = it % SM::NS;
+    mbar_wait(&full[s], (it / SM::NS) & 1);
+    T U[V][C], F[V][C], S_[V][C], G_[V][C];
+    {
+      const int sh = ((int)g.xo + xw) % SM::AL;
+      const T* st = stage + s * SM::STAGE + warp * C * SM::WB + sh + V * lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const VT uu = *reinterpret_cast<const VT*>(st + c * SM::WB);
+        if constexpr (V == 1) {
+          U[0][c] = uu;
+        } else {
+          U[0][c] = uu.x;
+          U[1][c] = uu.y;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int xv = xw + V * lane + v;
+      const int b = phys_flux<D, 0>(U[v], F[v], gm1);
+      bad |= ((xv >= -1) & (xv <= SX) & row_in) ? b : 0;
+    }
+    {
+      T Pin[C], Pnx[C], Un[C], Fn[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Un[c] = __shfl_down_sync(kFull, U[0][c], 1);
+        Fn[c] = __shfl_down_sync(kFull, F[0][c], 1);
+      }
+      force_face<D, 0>(U[V - 1], F[V - 1], Un, Fn, Pnx, qx, nqx, gm1);
+      if constexpr (V == 2) force_face<D, 0>(U[0], F[0], U[1], F[1], Pin, qx, nqx, gm1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const T Ppv = __shfl_up_sync(kFull, Pnx[c], 1);
+        if constexpr (V == 2) {
+          S_[0][c] = U[0][c] - (Pin[c] - Ppv);
+          S_[1][c] = U[1][c] - (Pnx[c] - Pin[c]);
+        } else {
+          S_[0][c] = U[0][c] - (Pnx[c] - Ppv);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int xv = xw + V * lane + v;
+      const int slot = V * lane + v;
+      const int b = phys_flux<D, 1>(S_[v], G_[v], gm1);
+      bad |= ((slot >= 1) & (slot <= W - 2) & (xv < SX) & row_in) ? b : 0;
+    }
+    // ---- publish (U*, F_y) of row `warp` (reader: warp+1)
+    if (warp <= NW - 2 && it >= 2) mbar_wait(&xyFree[p * NW + warp], (u - 1) & 1);
+    {
+      T* xr = xy + (p * NW + warp) * 2 * C * W + V * lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        VT sv, gv;
+        if constexpr (V == 1) {
+          sv = S_[0][c];
+          gv = G_[0][c];
+        } else {
+          sv.x = S_[0][c];
+          sv.y = S_[1][c];
+          gv.x = G_[0][c];
+          gv.y = G_[1][c];
+        }
+        *reinterpret_cast<VT*>(xr + c * W) = sv;
+        *reinterpret_cast<VT*>(xr + (C + c) * W) = gv;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&xyReady[p * NW + warp]);
+    // ---- y-face between rows warp-1 and warp (reader of the face: warp-1)
+    T Py[V][C];
+    if (warp >= 1) {
+      mbar_wait(&xyReady[p * NW + warp - 1], u & 1);
+      const T* pr = xy + (p * NW + warp - 1) * 2 * C * W + V * lane;
+      T Sp[V][C], Gp[V][C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const VT sv = *reinterpret_cast<const VT*>(pr + c * W);
+        const VT gv = *reinterpret_cast<const VT*>(pr + (C + c) * W);
+        if constexpr (V == 1) {
+          Sp[0][c] = sv;
+          Gp[0][c] = gv;
+        } else {
+          Sp[0][c] = sv.x;
+          Sp[1][c] = sv.y;
+          Gp[0][c] = gv.x;
+          Gp[1][c] = gv.y;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&xyFree[p * NW + warp - 1]);
+#pragma unroll
+      for (int v = 0; v < V; ++v) force_face<D, 1>(Sp[v], Gp[v], S_[v], G_[v], Py[v], qy, nqy, gm1);
+      if (warp >= 2 && it >= 2) mbar_wait(&fyFree[p * (NW - 1) + warp - 1], (u - 1) & 1);
+      T* fw = fy + (p * (NW - 1) + warp - 1) * C * W + V * lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        VT pv;
+        if constexpr (V == 1) {
+          pv = Py[0][c];
+        } else {
+          pv.x = Py[0][c];
+          pv.y = Py[1][c];
+        }
+        *reinterpret_cast<VT*>(fw + c * W) = pv;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fyReady[p * (NW - 1) + warp - 1]);
+    }
+    // ---- update rows 1..NW-2 with the face from warp+1
+    if (warp >= 1 && warp <= NW - 2) {
+      mbar_wait(&fyReady[p * (NW - 1) + warp], u & 1);
+      const T* fu = fy + (p * (NW - 1) + warp) * C * W + V * lane;
+      T o[V][C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const VT pv = *reinterpret_cast<const VT*>(fu + c * W);
+        if constexpr (V == 1) {
+          o[0][c] = S_[0][c] - (pv - Py[0][c]);
+        } else {
+          o[0][c] = S_[0][c] - (pv.x - Py[0][c]);
+          o[1][c] = S_[1][c] - (pv.y - Py[1][c]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&fyFree[p * (NW - 1) + warp]);
+      if (yr < SY) {
+        T* dst = a.out + g.row(yr, 0) * g.rstride + g.xo + xw + V * lane;
+        bool ok[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const int slot = V * lane + v;
+          ok[v] = (slot >= 1) & (slot <= W - 2) & (xw + slot < SX);
+        }
+        if constexpr (V == 2) {
+          if (ok[0] & ok[1]) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+              VT w;
+              w.x = o[0][c];
+              w.y = o[1][c];
+              *reinterpret_cast<VT*>(dst + c * g.cstride) = w;
+            }
+          } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+              if (ok[v])
+#pragma unroll
+                for (int c = 0; c < C; ++c) dst[c * g.cstride + v] = o[v][c];
+          }
+        } else {
+          if (ok[0])
+#pragma unroll
+            for (int c = 0; c < C; ++c) dst[c * g.cstride] = o[0][c];
+        }
+        const bool yface = (yr < g.pad) | (yr >= SY - g.pad);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          if (ok[v]) {
+            nan = max(nan, max(naninf(o[v][0]), naninf(o[v][C - 1])));
+            const int xv = xw + V * lane + v;
+            if (yface | (xv < g.pad) | (xv >= SX - g.pad)) images<D, 0>(a, xv, yr, 0, o[v]);
+          }
+        }
+      }
+    }
+  }
+  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+}
+
+template <typename T, int V, int NW, int MB>
+static void launch_pp2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  constexpr int W = 32 * V;
+  using SM = SmemPP<T, V, NW>;
+  const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
+  const int nyb = (int)((a.g.S[1] + (NW - 2) - 1) / (NW - 2));
+  const int ntiles = nwin * nyb;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(k_step2d_pp<T, V, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SM::bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step2d_pp<T, V, NW, MB>,
+                                                  32 * (NW + 1), SM::bytes());
+    if (per_sm < 1) per_sm = 1;
+  }
+  int nsm = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int grid = per_sm * nsm;
+  if (grid > ntiles) grid = ntiles;
+  k_step2d_pp<T, V, NW, MB><<<grid, 32 * (NW + 1), SM::bytes(), s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
+}
+
 // 2-D fused variants (RPL_VARIANT): 0/34 persistent TMA V=1 NW=8, 3 CTAs/SM
 // (default, fastest measured: 29.2 us at 1024^2 fp64), 32 same at 2 CTAs/SM,
 // 30 V=1 NW=16, 31 V=2 NW=8, 33 V=2 NW=16, 35/36 other occupancies;
@@ -1112,6 +1403,9 @@ int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
     case 40: case 41: *box_w = 32 + al; *box_rows = 8; return 1;
     case 42: *box_w = 64 + al; *box_rows = 8; return 1;
     case 43: *box_w = 32 + al; *box_rows = 16; return 1;
+    case 60: case 61: *box_w = 32 + al; *box_rows = 8; return 1;
+    case 62: *box_w = 32 + al; *box_rows = 16; return 1;
+    case 63: *box_w = 64 + al; *box_rows = 8; return 1;
     case 33: *box_w = 64 + al; *box_rows = 16; return 1;
     default: return 0;
   }
@@ -1268,6 +1562,10 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 33: return launch_pt2d<T, 2, 16>(a, tmap, s);
     case 0: case 34: return launch_pt2d<T, 1, 8, 3>(a, tmap, s);
     case 40: return launch_cm2d<T, 1, 8, 3>(a, tmap, s);
+    case 60: return launch_pp2d<T, 1, 8, 3>(a, tmap, s);
+    case 61: return launch_pp2d<T, 1, 8, 2>(a, tmap, s);
+    case 62: return launch_pp2d<T, 1, 16, 1>(a, tmap, s);
+    case 63: return launch_pp2d<T, 2, 8, 2>(a, tmap, s);
     case 41: return launch_cm2d<T, 1, 8, 2>(a, tmap, s);
     case 42: return launch_cm2d<T, 2, 8, 2>(a, tmap, s);
     case 43: return launch_cm2d<T, 1, 16, 1>(a, tmap, s);

@@ -20,7 +20,7 @@ bad = np.argwhere(np.any(a != b, axis=-1))
 print("EQUAL" if len(bad) == 0 else f"DIFF n={len(bad)} first={bad[:3].tolist()} last={bad[-3:].tolist()}")
 '''
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-for var in ["40", "41", "42", "43"]:
+for var in os.environ.get("VARS", "40").split(","):
     for n in ["130,70", "256,256", "1024,1024"]:
         for rows in [0, 8, 16]:
             env = dict(os.environ, ROOT=root, N=n, ROWS=str(rows), RPL_VARIANT=var)
