@@ -42,6 +42,13 @@ WORKLOADS = {
                  label="3-D Euler FORCE 384^3/GPU fp32 blocks (BASELINE configs[3])"),
     "l256": dict(ndim=3, n=(256, 256, 256), dtype="f32", scaling="weak",
                  label="3-D Euler FORCE 256^3 (BASELINE configs[4])"),
+    # the paper's own 2-D scaling problems
+    "p6400": dict(ndim=2, n=(6400, 4000), dtype="f64", scaling="strong",
+                  label="2-D Euler FORCE 6400x4000 fp64, y-split (paper strong 'small', P:1407)"),
+    "p9600": dict(ndim=2, n=(9600, 6000), dtype="f64", scaling="strong",
+                  label="2-D Euler FORCE 9600x6000 fp64, y-split (paper strong 'large', P:1408)"),
+    "pweak": dict(ndim=2, n=(2560, 2500), dtype="f64", scaling="weak",
+                  label="2-D Euler FORCE 6.4M cells/GPU fp64, y-split (paper weak, P:1393-1402)"),
 }
 W384_BLOCKS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
 
