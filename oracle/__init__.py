@@ -16,6 +16,8 @@ Parity status per function:
   max_wavespeed               -- pinned (closed-form states)
   riemann_exact               -- pinned (textbook star state, RH jump conditions)
   run_cfl                     -- pinned through P2 (Sod convergence)
+  flux_difference             -- pinned (uniform state -> 0, Fourier symbol of the
+                                 linear FORCE flux difference, 1-D sweep relation)
 """
 from __future__ import annotations
 
@@ -74,6 +76,8 @@ def _L():
         _lib.orc_run_cfl_f64.argtypes = [gp, dp, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                          ctypes.c_double, ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_int)]
+        _lib.orc_flux_difference_f64.argtypes = [gp, dp, ctypes.c_double, dp]
+        _lib.orc_flux_difference_f32.argtypes = [gp, fp, ctypes.c_double, fp]
         _lib.orc_riemann_exact.argtypes = [ctypes.c_double] * 7 + [dp, ctypes.c_long, dp, dp]
     return _lib
 
@@ -161,6 +165,20 @@ def fill_ghosts(grid: Grid, P: np.ndarray) -> np.ndarray:
     assert P.shape == padded_shape(grid)
     _L().orc_fill_ghosts_f64(ctypes.byref(grid._c()), _arr(P, np.float64))
     return P
+
+
+def flux_difference(grid: Grid, U: np.ndarray, dt: float) -> np.ndarray:
+    """R = sum_d (F_{i+1/2} - F_{i-1/2}) with FORCE (paper sec. 7.3, Table 4 kernel)."""
+    U = np.ascontiguousarray(U)
+    R = np.empty_like(U)
+    g = grid._c()
+    if U.dtype == np.float64:
+        _check(_L().orc_flux_difference_f64(ctypes.byref(g), _arr(U, np.float64), float(dt),
+                                            _arr(R, np.float64)))
+    else:
+        _check(_L().orc_flux_difference_f32(ctypes.byref(g), _arr(U, np.float32), float(dt),
+                                            _arr(R, np.float32)))
+    return R
 
 
 def max_wavespeed(grid: Grid, U: np.ndarray) -> float:

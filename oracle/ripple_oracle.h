@@ -51,6 +51,11 @@ int orc_sweep_f64(const orc_grid* g, double* U, double dt, int d);
  * dims in order 0..ndim-1 over the full padded extent. For tests. */
 void orc_fill_ghosts_f64(const orc_grid* g, double* P);
 
+/* Flux difference (paper sec. 7.3): R = sum_d (F_{i+1/2} - F_{i-1/2})
+ * with FORCE at step dt on every face of every interior cell (one ghost fill). */
+int orc_flux_difference_f64(const orc_grid* g, const double* U, double dt, double* R);
+int orc_flux_difference_f32(const orc_grid* g, const float* U, double dt, float* R);
+
 /* S = max over interior cells of |u| + c, c = sqrt(gamma p / rho). */
 double orc_max_wavespeed_f64(const orc_grid* g, const double* U);
 double orc_max_wavespeed_f32(const orc_grid* g, const float* U);

@@ -45,7 +45,8 @@ EXPORTS = ["rpl_config_init", "rpl_config_check", "rpl_arena_bytes", "rpl_nccl_u
            "rpl_create", "rpl_local_box", "rpl_set_state", "rpl_get_state", "rpl_get_padded",
            "rpl_fill_padding", "rpl_advance", "rpl_max_wavespeed", "rpl_advance_cfl",
            "rpl_synchronize", "rpl_launches_per_step", "rpl_profile", "rpl_profile_read",
-           "rpl_halo_plan", "rpl_p2p_export", "rpl_p2p_attach", "rpl_destroy",
+           "rpl_halo_plan", "rpl_p2p_export", "rpl_p2p_attach",
+           "rpl_flux_difference", "rpl_get_flux_difference", "rpl_destroy",
            "rpl_last_error"]
 
 _lib = None
@@ -84,6 +85,8 @@ def lib():
     L.rpl_halo_plan.argtypes = [P(Config), P(HaloEdge), ctypes.c_int32, P(ctypes.c_int32)]
     L.rpl_p2p_export.argtypes = [vp, vp, P(ctypes.c_size_t)]
     L.rpl_p2p_attach.argtypes = [vp, vp, ctypes.c_size_t]
+    L.rpl_flux_difference.argtypes = [vp, ctypes.c_double]
+    L.rpl_get_flux_difference.argtypes = [vp, vp]
     L.rpl_destroy.argtypes = [vp]
     L.rpl_destroy.restype = None
     L.rpl_last_error.argtypes = []

@@ -1400,6 +1400,8 @@ int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
     case 31: *box_w = 64 + al; *box_rows = 8; return 1;
     case 0: case 32: case 34: case 35: *box_w = 32 + al; *box_rows = 8; return 1;
     case 36: *box_w = 64 + al; *box_rows = 8; return 1;
+    case 37: case 39: *box_w = 32 + al; *box_rows = 12; return 1;
+    case 38: *box_w = 32 + al; *box_rows = 10; return 1;
     case 40: case 41: *box_w = 32 + al; *box_rows = 8; return 1;
     case 42: *box_w = 64 + al; *box_rows = 8; return 1;
     case 43: *box_w = 32 + al; *box_rows = 16; return 1;
@@ -1571,6 +1573,9 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 43: return launch_cm2d<T, 1, 16, 1>(a, tmap, s);
     case 35: return launch_pt2d<T, 1, 8, 4>(a, tmap, s);
     case 36: return launch_pt2d<T, 2, 8, 2>(a, tmap, s);
+    case 37: return launch_pt2d<T, 1, 12, 2>(a, tmap, s);
+    case 38: return launch_pt2d<T, 1, 10, 3>(a, tmap, s);
+    case 39: return launch_pt2d<T, 1, 12, 3>(a, tmap, s);
     default: break;
   }
   KArgs<T> am = a;
@@ -1624,5 +1629,85 @@ template void launch_maxws<float>(const Geom&, const float*, double, unsigned lo
                                   unsigned*, cudaStream_t);
 template void launch_maxws<double>(const Geom&, const double*, double, unsigned long long*,
                                    unsigned*, cudaStream_t);
+
+}  // namespace rpl
+
+namespace rpl {
+
+// ---------------------------------------------------------------------------
+// Flux difference (sec. 7.3): the paper's
+// single-GPU FV benchmark (Table 4).  For every interior cell
+//   R = sum_d (F_{i+1/2,d} - F_{i-1/2,d}),   F = Toro's FORCE flux at step dt,
+// "performed for all four faces of each cell": thread per cell,
+// both faces of every direction evaluated by the cell (the paper's algorithm,
+// not the shared-face scheme of the step kernels).  Reads the current state
+// (ghosts filled), writes R to the scratch buffer.
+// ---------------------------------------------------------------------------
+template <typename T, int D, int L>
+__global__ void __launch_bounds__(256) k_fluxdiff(const __grid_constant__ KArgs<T> a) {
+  constexpr int C = D + 2;
+  const Geom& g = a.g;
+  const int64_t n = g.cells();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = i % g.S[0];
+    const int64_t y = (i / g.S[0]) % g.S[1];
+    const int64_t z = i / (g.S[0] * g.S[1]);
+    T U0[C], R[C];
+    load_cell<D, L>(g, a.in, x, y, z, U0);
+#pragma unroll
+    for (int c = 0; c < C; ++c) R[c] = T(0);
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int64_t dx = d == 0, dy = d == 1, dz = d == 2;
+      T Um[C], Up[C], Fm[C], F0[C], Fp[C], PL[C], PR[C];
+      load_cell<D, L>(g, a.in, x - dx, y - dy, z - dz, Um);
+      load_cell<D, L>(g, a.in, x + dx, y + dy, z + dz, Up);
+      const T inv_lam = T(0.25) / a.q[d];  // 1/lam: Phi = lam F_FORCE
+      if (d == 0) {
+        phys_flux<D, 0>(Um, Fm, a.gm1);
+        phys_flux<D, 0>(U0, F0, a.gm1);
+        phys_flux<D, 0>(Up, Fp, a.gm1);
+        force_face<D, 0>(Um, Fm, U0, F0, PL, a.q[0], a.nq2[0], a.gm1);
+        force_face<D, 0>(U0, F0, Up, Fp, PR, a.q[0], a.nq2[0], a.gm1);
+      } else if (d == 1) {
+        if constexpr (D > 1) {
+          phys_flux<D, 1>(Um, Fm, a.gm1);
+          phys_flux<D, 1>(U0, F0, a.gm1);
+          phys_flux<D, 1>(Up, Fp, a.gm1);
+          force_face<D, 1>(Um, Fm, U0, F0, PL, a.q[1], a.nq2[1], a.gm1);
+          force_face<D, 1>(U0, F0, Up, Fp, PR, a.q[1], a.nq2[1], a.gm1);
+        }
+      } else {
+        if constexpr (D > 2) {
+          phys_flux<D, 2>(Um, Fm, a.gm1);
+          phys_flux<D, 2>(U0, F0, a.gm1);
+          phys_flux<D, 2>(Up, Fp, a.gm1);
+          force_face<D, 2>(Um, Fm, U0, F0, PL, a.q[2], a.nq2[2], a.gm1);
+          force_face<D, 2>(U0, F0, Up, Fp, PR, a.q[2], a.nq2[2], a.gm1);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) R[c] = fma(PR[c] - PL[c], inv_lam, R[c]);
+    }
+    store_cell<D, L>(g, a.out, x, y, z, R);
+  }
+}
+
+template <typename T>
+void launch_fluxdiff(const KArgs<T>& a, cudaStream_t s) {
+  int64_t b = (a.g.cells() + 255) / 256;
+  if (b > 148 * 32) b = 148 * 32;
+  const int grid = (int)(b < 1 ? 1 : b);
+  const int D = a.g.D, L = a.g.layout;
+#define RPL_FD(DD, LL) k_fluxdiff<T, DD, LL><<<grid, 256, 0, s>>>(a)
+  if (D == 1) { if (L == 0) RPL_FD(1, 0); else RPL_FD(1, 1); }
+  if (D == 2) { if (L == 0) RPL_FD(2, 0); else RPL_FD(2, 1); }
+  if (D == 3) { if (L == 0) RPL_FD(3, 0); else RPL_FD(3, 1); }
+#undef RPL_FD
+}
+
+template void launch_fluxdiff<float>(const KArgs<float>&, cudaStream_t);
+template void launch_fluxdiff<double>(const KArgs<double>&, cudaStream_t);
 
 }  // namespace rpl

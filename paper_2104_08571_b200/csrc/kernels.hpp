@@ -26,6 +26,9 @@ template <typename T>
 void launch_maxws(const Geom& g, const T* in, double gamma, unsigned long long* smax,
                   unsigned* flag, cudaStream_t s);
 
+template <typename T>
+void launch_fluxdiff(const KArgs<T>& a, cudaStream_t s);  // sec. 7.3 flux difference (f2)
+
 int auto_rows_2d(const Geom& g);
 int auto_rows_3d(const Geom& g);
 

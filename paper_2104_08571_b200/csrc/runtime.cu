@@ -516,7 +516,7 @@ extern "C" rpl_status rpl_local_box(const rpl_domain* d, int64_t lo[3], int64_t 
 }
 
 // host box <-> partition interior copies (dense SoA host [C][bz][by][bx])
-static rpl_status xfer(rpl_domain* d, void* host, bool to_dev) {
+static rpl_status xfer(rpl_domain* d, void* host, bool to_dev, int which = -1) {
   const Geom& g = d->g;
   int64_t lo[3], hi[3];
   rpl_local_box(d, lo, hi);
@@ -526,7 +526,7 @@ static rpl_status xfer(rpl_domain* d, void* host, bool to_dev) {
     int pc[3];
     g.part_coords(p, pc);
     const int64_t o[3] = {pc[0] * g.S[0] - lo[0], pc[1] * g.S[1] - lo[1], pc[2] * g.S[2] - lo[2]};
-    char* dev = (char*)d->buf[d->cur][p];
+    char* dev = (char*)d->buf[which < 0 ? d->cur : which][p];
     if (g.layout == 0) {
       for (int c = 0; c < g.C; ++c) {
         cudaMemcpy3DParms m;
@@ -967,5 +967,51 @@ extern "C" rpl_status rpl_p2p_attach(rpl_domain* d, const void* blobs, size_t bl
   CU(cudaMemcpy(d->d_tab, d->buf, sizeof(void*) * 2 * kMaxParts, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d->d_peer_ctl, ctl, sizeof(void*) * kMaxParts, cudaMemcpyHostToDevice));
   d->p2p_attached = true;
+  return RPL_OK;
+}
+
+// ------------------------------------------------------------------ flux difference (f2)
+template <typename T>
+static rpl_status fluxdiff_t(rpl_domain* d, double dt) {
+  const Geom& g = d->g;
+  KArgs<T> a;
+  memset(&a, 0, sizeof(a));
+  a.g = g;
+  for (int k = 0; k < 3; ++k) {
+    const double lam = k < g.D ? dt / d->cfg.dx[k] : 1.0;
+    a.q[k] = (T)(0.25 * lam);
+    a.nq2[k] = (T)(-0.25 * lam * lam);
+  }
+  a.gm1 = (T)(d->cfg.gamma - 1.0);
+  a.flag = d->d_flag;
+  for (int p : d->local) {
+    a.part = p;
+    g.part_coords(p, a.pc);
+    for (int k = 0; k < 3; ++k) a.lo[k] = a.pc[k] * g.S[k];
+    a.in = (const T*)d->buf[d->cur][p];
+    a.out = (T*)d->buf[d->cur ^ 1][p];
+    launch_fluxdiff<T>(a, d->stream);
+  }
+  CU(cudaGetLastError());
+  return RPL_OK;
+}
+
+extern "C" rpl_status rpl_flux_difference(rpl_domain* d, double dt) {
+  if (!d) return fail(RPL_E_INVALID_ARG, "null domain");
+  if (!(dt > 0.0)) return fail(RPL_E_INVALID_ARG, "dt must be > 0");
+  CU(cudaSetDevice(d->device));
+  if (d->ghosts_stale) {
+    rpl_status st = rpl_fill_padding(d);
+    if (st) return st;
+  }
+  return d->g.elem == 8 ? fluxdiff_t<double>(d, dt) : fluxdiff_t<float>(d, dt);
+}
+
+extern "C" rpl_status rpl_get_flux_difference(rpl_domain* d, void* host) {
+  if (!d || !host) return fail(RPL_E_INVALID_ARG, "null argument");
+  CU(cudaSetDevice(d->device));
+  rpl_status st = xfer(d, host, false, d->cur ^ 1);
+  if (st) return st;
+  CU(cudaStreamSynchronize(d->stream));
   return RPL_OK;
 }

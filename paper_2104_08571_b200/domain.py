@@ -187,6 +187,15 @@ class Domain:
     def synchronize(self):
         N.check(N.lib().rpl_synchronize(self._h))
 
+    # -- paper sec. 7.3 flux difference (Table 4 benchmark)
+    def flux_difference(self, dt: float):
+        N.check(N.lib().rpl_flux_difference(self._h, float(dt)))
+
+    def get_flux_difference(self) -> np.ndarray:
+        soa = np.empty(self.soa_shape(), dtype=self.np_dtype)
+        N.check(N.lib().rpl_get_flux_difference(self._h, soa.ctypes.data))
+        return np.ascontiguousarray(np.moveaxis(soa, 0, -1))
+
     # -- P2P transport (nranks > 1): export IPC blob, all-gather it, attach
     def p2p_export(self) -> bytes:
         n = ctypes.c_size_t(0)

@@ -400,3 +400,46 @@ def test_fp32_tracks_fp64_on_shock_bubble():
     scale = np.max(np.abs(a), axis=(0, 1))
     scale[2] = scale[1]  # m_y is a tiny perturbation-driven field: measure against |m|
     assert np.all(err / scale < 1e-5), err / scale
+
+
+# ---------------------------------------------------------------- flux difference (sec. 7.3)
+def test_flux_difference_uniform_is_zero():
+    """a uniform state has zero flux difference (bitwise)."""
+    for n in [(9,), (7, 6), (5, 4, 6)]:
+        g = oracle.Grid(n, pad=2, bc_lo=[oracle.BC_PERIODIC] * len(n),
+                        bc_hi=[oracle.BC_PERIODIC] * len(n))
+        U = W.uniform(n, rho=0.7, vel=[0.3, -0.2, 0.1][:len(n)], p=1.1)
+        assert np.all(oracle.flux_difference(g, U, 0.01) == 0.0)
+
+
+@pytest.mark.parametrize("n,vel,k", [((48,), [0.6], [3]), ((32, 24), [0.5, -0.4], [2, 3])])
+def test_flux_difference_fourier_symbol(n, vel, k):
+    """On the density-wave manifold F(U) = uU + const, so FORCE's flux difference of a
+    Fourier mode is the closed form (unsplit sum over dims):
+      R_hat = sum_d [ i u_d sin(th_d) + 1/2 (dx_d/dt + dt u_d^2/dx_d)(1 - cos(th_d)) ] U_hat."""
+    D = len(n)
+    per = [oracle.BC_PERIODIC] * D
+    g = oracle.Grid(n, pad=2, bc_lo=per, bc_hi=per)
+    U0 = W.smooth_density_wave(n, vel=vel, amp=0.2, k=k)
+    dt = 0.3 / max(n)
+    R = oracle.flux_difference(g, U0, dt)
+    r_hat = np.fft.fftn(R[..., 0])
+    u_hat = np.fft.fftn(U0[..., 0] - 1.0)
+    idx = tuple([k[d] % n[d] for d in reversed(range(D))])
+    sym = 0j
+    for d in range(D):
+        th = 2 * math.pi * k[d] / n[d]
+        dx = g.dx[d]
+        sym += 1j * vel[d] * math.sin(th) + 0.5 * (dx / dt + dt * vel[d] ** 2 / dx) * (1 - math.cos(th))
+    assert abs(r_hat[idx] - sym * u_hat[idx]) <= 1e-10 * abs(sym * u_hat[idx])
+
+
+def test_flux_difference_is_the_1d_sweep_increment():
+    """In 1-D one split sweep is U' = U - (dt/dx) R."""
+    n = (40,)
+    g = oracle.Grid(n, pad=2)
+    U = W.sod(40)
+    dt = 0.4 / 40 / 2.5
+    R = oracle.flux_difference(g, U, dt)
+    Us = oracle.sweep(g, U, dt, 0)
+    assert np.allclose(Us, U - (dt * 40) * R, rtol=0, atol=1e-14)

@@ -292,3 +292,27 @@ def test_fused3d_aos_equals_soa_bitwise(dtype):
     b = run_gpu(U0, 1e-4, 8, layout="aos", **kw)
     c = run_gpu(U0, 1e-4, 8, layout="aos", kernel="split", **kw)
     assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-10), ("f32", 1e-4)])
+@pytest.mark.parametrize("n", [(200,), (130, 70), (40, 30, 20)])
+def test_flux_difference_matches_oracle(dtype, tol, n):
+    """Paper sec. 7.3 kernel (Table 4): GPU flux difference vs the oracle's."""
+    D = len(n)
+    dx = [1.0 / n[0]] * D
+    U0 = W.shock_bubble(n, dx=dx) if D > 1 else W.sod(n[0])
+    if dtype == "f32":
+        U0 = U0.astype(np.float32)
+    bl = ["reflective", "periodic", "clamp"][:D]
+    bh = ["clamp", "periodic", "reflective"][:D]
+    dt = 1e-4
+    with R.Domain(n, dtype=dtype, dx=dx, bc_lo=bl, bc_hi=bh) as dom:
+        dom.set_state(U0)
+        dom.flux_difference(dt)
+        Rg = dom.get_flux_difference()
+        assert np.array_equal(dom.get_state(), U0)  # the state is unchanged
+    g = oracle.Grid(n, pad=2, dx=dx, bc_lo=[OK[b] for b in bl], bc_hi=[OK[b] for b in bh])
+    Ro = oracle.flux_difference(g, U0, dt)
+    # R is a difference of O(1) fluxes: measure against the flux scale, not R itself
+    scale = np.max(np.abs(U0.astype(np.float64))) / min(dx) * 10
+    assert np.max(np.abs(Rg.astype(np.float64) - Ro.astype(np.float64))) <= tol * scale
