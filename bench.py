@@ -50,6 +50,14 @@ WORKLOADS = {
     "pweak": dict(ndim=2, n=(2560, 2500), dtype="f64", scaling="weak",
                   label="2-D Euler FORCE 6.4M cells/GPU fp64, y-split (paper weak, P:1393-1402)"),
 }
+# the paper's Table 4 (sec. 7.3) flux difference, strided layout,
+# one pass over (k*1024)^2 cells; paper V100 times (ms) as context.
+PAPER_TABLE4_MS = {1: 0.0757, 2: 0.2438, 4: 0.9101, 8: 3.5533, 16: 14.282, 32: 59.028}
+for _k in PAPER_TABLE4_MS:
+    WORKLOADS[f"fd{_k}k"] = dict(
+        ndim=2, n=(_k * 1024, _k * 1024), dtype="f32", scaling="weak", op="fluxdiff",
+        pad=1, paper_ms=PAPER_TABLE4_MS[_k],
+        label=f"sec. 7.3 flux difference {_k}k^2 fp32 SoA (paper Table 4, Size^2 = {_k}k)")
 W384_BLOCKS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
 
 
@@ -115,6 +123,14 @@ class Clocks:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.samples)}
+
+
+def N_get_fd(dom, ptr):
+    """rpl_get_flux_difference into a raw host pointer (e2e of the flux-difference op)."""
+    import ctypes
+
+    from paper_2104_08571_b200 import _native as N
+    N.check(N.lib().rpl_get_flux_difference(dom._h, ctypes.c_void_p(ptr)))
 
 
 def measured_peak_gbs():
@@ -274,7 +290,9 @@ def main():
             idt.copy_(torch.frombuffer(bytearray(R.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().numpy().tobytes())
-    dom = R.Domain(gn, pad=2, parts=parts, dtype=wl["dtype"], kernel=args.kernel, dx=dx,
+    op = wl.get("op", "step")
+    dom = R.Domain(gn, pad=wl.get("pad", 2), parts=parts, dtype=wl["dtype"], kernel=args.kernel,
+                   dx=dx,
                    layout=args.layout,
                    nranks=world, rank=rank if world > 1 else 0, nccl_id=nccl_id, device=dev,
                    stream=stream.cuda_stream, rows_per_chunk=args.rows,
@@ -330,7 +348,10 @@ def main():
         torch.cuda._sleep(200_000 * nsteps)
         for k in range(nsteps):
             ev[k][0].record(stream)
-            dom.advance(dt, 1)
+            if op == "fluxdiff":
+                dom.flux_difference(dt)
+            else:
+                dom.advance(dt, 1)
             ev[k][1].record(stream)
             do_flush()
         torch.cuda.synchronize()
@@ -370,8 +391,12 @@ def main():
         e0.record(stream)
         for _ in range(args.e2e_steps):
             dom.set_state_ptr(h_in.data_ptr())
-            dom.advance(dt, 1)
-            dom.get_state_ptr(h_out.data_ptr())
+            if op == "fluxdiff":
+                dom.flux_difference(dt)
+                N_get_fd(dom, h_out.data_ptr())
+            else:
+                dom.advance(dt, 1)
+                dom.get_state_ptr(h_out.data_ptr())
         e1.record(stream)
         torch.cuda.synchronize()
         te = e0.elapsed_time(e1) / 1e3
@@ -386,9 +411,14 @@ def main():
                "path": "rpl_set_state(pinned host) + rpl_advance(dt,1) + rpl_get_state(pinned host)"}
 
     value = global_cells * args.steps / t_total / 1e9
+    if op == "fluxdiff":  # one kernel per call: the step events time the launch
+        kern_ms, kern_launches = t_total * 1e3, args.steps
+        launches_per_step = 1
     peak, peak_src = measured_peak_gbs()
     alg_bytes = 2 * C * elem * local_cells  # per step-kernel launch (one partition per rank)
     kname = {"fused": {1: "k_sweep", 2: "k_step2d_pt", 3: "k_step3d"}[D], "split": "k_sweep"}[args.kernel]
+    if op == "fluxdiff":
+        kname = "k_fluxdiff"
     per_launch_ms = kern_ms / max(kern_launches, 1)
     launches_per_step_kernel = max(1, kern_launches // max(5, min(args.steps, 20)))
     if args.kernel == "split" or D != 2:
@@ -403,10 +433,15 @@ def main():
             "alg_bytes_per_launch": alg_bytes_launch, "launch_ms": per_launch_ms,
             "launches_per_step": launches_per_step_kernel,
             "frac_of_8TBs": achieved / 8000.0}
-    line = {"metric": "Gcell-updates/s", "value": value, "unit": "Gcell-updates/s",
+    vs = None
+    if op == "fluxdiff" and wl.get("paper_ms"):
+        # paper Table 4 (V100, strided) time for the same pass: context, other hardware
+        vs = wl["paper_ms"] / (t_total / args.steps * 1e3)
+    line = {"metric": "Gcell-updates/s" if op == "step" else "Gcell/s (flux difference)",
+            "value": value, "unit": "Gcell-updates/s" if op == "step" else "Gcell/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True,
-            "scaling": wl["scaling"], "vs_baseline": None, "dtype": wl["dtype"],
+            "scaling": wl["scaling"], "vs_baseline": vs, "dtype": wl["dtype"],
             "data": "synthetic",
             "config": {"workload": wl["label"], "global_cells": gn, "parts": parts,
                        "kernel": args.kernel, "layout": args.layout,
@@ -414,7 +449,8 @@ def main():
                        "l2": "flushed between steps (256 MiB write), per-step CUDA events"
                              if flush is not None else "not flushed",
                        "timing": "sum of per-step CUDA events on the library stream, max over ranks",
-                       "wall_s": wall, "dt": dt, "S0": S0},
+                       "wall_s": wall, "dt": dt, "S0": S0, "op": op,
+                       "paper_v100_ms": wl.get("paper_ms")},
             "roofline": roof, "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary()}
     if e2e:
