@@ -18,6 +18,9 @@ Parity status per function:
   run_cfl                     -- pinned through P2 (Sod convergence)
   flux_difference             -- pinned (uniform state -> 0, Fourier symbol of the
                                  linear FORCE flux difference, 1-D sweep relation)
+  step/sweep with order=2     -- pinned (limiter-inactive data == order 1 bitwise,
+    (MUSCL-Hancock + FORCE)      L1 rate ~2 on a smooth wave, Sod bounds/convergence,
+                                 conservation, symmetry, uniform state)
 """
 from __future__ import annotations
 
@@ -52,7 +55,8 @@ def build(force: bool = False) -> str:
 class _Grid(ctypes.Structure):
     _fields_ = [("ndim", ctypes.c_int), ("n", ctypes.c_long * 3), ("pad", ctypes.c_int),
                 ("dx", ctypes.c_double * 3), ("gamma", ctypes.c_double),
-                ("bc_lo", ctypes.c_int * 3), ("bc_hi", ctypes.c_int * 3)]
+                ("bc_lo", ctypes.c_int * 3), ("bc_hi", ctypes.c_int * 3),
+                ("order", ctypes.c_int)]
 
 
 _lib = None
@@ -85,7 +89,7 @@ def _L():
 class Grid:
     """Geometry + scheme constants (SURVEY 8(c) input line)."""
 
-    def __init__(self, n, pad=2, dx=None, gamma=1.4, bc_lo=None, bc_hi=None):
+    def __init__(self, n, pad=2, dx=None, gamma=1.4, bc_lo=None, bc_hi=None, order=1):
         n = tuple(int(v) for v in n)
         self.ndim = len(n)
         assert 1 <= self.ndim <= 3
@@ -95,6 +99,7 @@ class Grid:
         self.gamma = float(gamma)
         self.bc_lo = tuple(bc_lo if bc_lo is not None else [BC_TRANSMISSIVE] * self.ndim)
         self.bc_hi = tuple(bc_hi if bc_hi is not None else [BC_TRANSMISSIVE] * self.ndim)
+        self.order = int(order)
 
     @property
     def C(self):
@@ -114,6 +119,7 @@ class Grid:
             g.bc_hi[d] = self.bc_hi[d] if d < self.ndim else 0
         g.pad = self.pad
         g.gamma = self.gamma
+        g.order = self.order
         return g
 
 

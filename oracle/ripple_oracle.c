@@ -30,6 +30,7 @@
 
 int orc_sweep_f64(const orc_grid* g, double* U, double dt, int d) {
   if (!g || d < 0 || d >= g->ndim) return ORC_E_INVALID;
+  if (g->order == 2 && g->pad < 2) return ORC_E_INVALID;
   int C = g->ndim + 2;
   size_t n = padded_cells_f64(g) * (size_t)C;
   double* a = (double*)calloc(n, sizeof(double));

@@ -18,8 +18,14 @@
  *   ((k*n[1] + j)*n[0] + i)*C + c,   C = ndim + 2,  x fastest.
  * The oracle allocates its own padded copy internally.
  *
+ * Order 2 (the paper is silent on reconstruction order, Listing 8 is
+ * order 1): per sweep, per cell, minmod-limited slopes of the conserved variables,
+ * boundary-extrapolated values, a half-step (dt/2) evolution with the physical
+ * flux, FORCE at every face between the evolved values (Toro's SLIC scheme).
+ *
  * Return codes: 0 = ok, -7 = numerical-domain error (rho<=0, p<=0 or non-finite
- * after a sweep), -1 = invalid argument.
+ * after a sweep; order 2 also: rho<=0 or p<=0 in an extrapolated or
+ * evolved boundary value), -1 = invalid argument.
  */
 #ifndef RIPPLE_ORACLE_H
 #define RIPPLE_ORACLE_H
@@ -38,6 +44,9 @@ typedef struct {
   double gamma;      /* ratio of specific heats (1.4) */
   int bc_lo[3];      /* boundary kind on the low face of each dim */
   int bc_hi[3];      /* boundary kind on the high face of each dim */
+  int order;         /* 1: piecewise constant (reading S7; 0 also means 1);
+                      * 2: MUSCL-Hancock + FORCE = Toro's SLIC (SURVEY f3,
+                      *    DESIGN.md readings F3a-F3d), needs pad >= 2 */
 } orc_grid;
 
 /* nsteps split FORCE steps with fixed dt (reading D3).  U in/out. */

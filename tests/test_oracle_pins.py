@@ -443,3 +443,136 @@ def test_flux_difference_is_the_1d_sweep_increment():
     R = oracle.flux_difference(g, U, dt)
     Us = oracle.sweep(g, U, dt, 0)
     assert np.allclose(Us, U - (dt * 40) * R, rtol=0, atol=1e-14)
+
+
+# ---------------------------------------------------------------- order 2
+# MUSCL-Hancock + FORCE (Toro's SLIC, "Riemann Solvers ...", secs. 14.4, 14.5.3)
+# with the minmod limiter (reading F3a).
+def _slic_exp_symbol(z, c):
+    """Amplification of one SLIC step for linear advection (speed a, c = a dt/dx) on
+    an exponential mode v_i = z**i, z > 0 real, z != 1.  On such a mode minmod
+    always selects the same one-sided difference: the backward one for z > 1
+    (|1 - 1/z| < |z - 1|), the forward one for z < 1, so Delta_i = beta v_i with
+    beta = 1 - 1/z or z - 1.  Derived from the textbook definitions:
+      Ubar^R_i     = v_i + (1 - c) Delta_i / 2            (= v_i r)
+      Ubar^L_{i+1} = v_{i+1} - (1 + c) Delta_{i+1} / 2    (= v_i z l)
+      (dt/dx) F^FORCE(L, R) = c (L + R) / 2 - (1 + c^2) (R - L) / 4   (linear flux)
+      G = 1 - phi (1 - 1/z),  phi = (dt/dx) F_{i+1/2} / v_i."""
+    beta = (1.0 - 1.0 / z) if z > 1.0 else (z - 1.0)
+    r = 1.0 + 0.5 * (1.0 - c) * beta
+    l = 1.0 - 0.5 * (1.0 + c) * beta
+    phi = 0.5 * c * (r + z * l) - 0.25 * (1.0 + c * c) * (z * l - r)
+    return 1.0 - phi * (1.0 - 1.0 / z)
+
+
+@pytest.mark.parametrize("z,a", [(1.06, 0.7), (1.06, -0.5), (0.93, 0.6), (0.93, -0.8)])
+def test_order2_exponential_mode_symbol(z, a):
+    """Density mode rho = 1 + eps z**i at constant u = a, p = 1 (the contact manifold,
+    where F(U) = a U + const and the componentwise minmod slopes stay on the
+    manifold): interior cells (outside the boundaries' domain of dependence, two
+    cells per sweep) follow the closed-form symbol."""
+    N, nsteps, eps, gam = 120, 5, 1e-3, 1.4
+    i = np.arange(N)
+    v = eps * z ** (i - N / 2)
+    rho = 1.0 + v
+    U0 = np.stack([rho, a * rho, 1.0 / (gam - 1.0) + 0.5 * a * a * rho], axis=-1)
+    grid = oracle.Grid((N,), pad=2, dx=[1.0 / N], order=2)
+    dt = 0.6 / N / (abs(a) + 1.0)
+    c = a * dt / grid.dx[0]
+    U = oracle.step(grid, U0, dt, nsteps)
+    G = _slic_exp_symbol(z, c)
+    m = slice(2 * nsteps + 4, N - 2 * nsteps - 4)
+    got = U[m, 0] - 1.0
+    want = v[m] * G ** nsteps
+    assert np.max(np.abs(got - want) / np.abs(want)) <= 1e-10
+    # and differs from the order-1 symbol (the reconstruction is active)
+    U1 = oracle.step(oracle.Grid((N,), pad=2, dx=[1.0 / N]), U0, dt, nsteps)
+    assert np.max(np.abs(U1[m, 0] - U[m, 0])) > 1e-3 * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("n", [(64,), (12, 10)])
+def test_order2_limiter_inactive_equals_order1_bitwise(n):
+    """Alternating (checkerboard) data has an extremum in every cell: minmod gives
+    zero slopes, U^L = U^R = U, the half step cancels, and SLIC is FORCE."""
+    D = len(n)
+    idx = np.indices(tuple(reversed(n))).sum(axis=0)
+    sign = np.where(idx % 2 == 0, 1.0, -1.0)
+    U0 = W.uniform(n)
+    U0[..., 0] += 0.05 * sign
+    U0[..., D + 1] += 0.1 * sign
+    per = [oracle.BC_PERIODIC] * D
+    dt = 0.2 / max(n)
+    # one sweep in x (data alternates along every dim, so x slopes are zero)
+    g1 = oracle.Grid(n, pad=2, bc_lo=per, bc_hi=per)
+    g2 = oracle.Grid(n, pad=2, bc_lo=per, bc_hi=per, order=2)
+    assert np.array_equal(oracle.sweep(g1, U0, dt, 0), oracle.sweep(g2, U0, dt, 0))
+    # a monotone ramp on top activates the slopes: the two orders then differ
+    ramp = U0 + 0.1 * np.linspace(0.0, 1.0, U0.size).reshape(U0.shape)
+    assert not np.array_equal(oracle.sweep(g1, ramp, dt, 0), oracle.sweep(g2, ramp, dt, 0))
+
+
+def test_order2_smooth_wave_converges_at_second_order():
+    errs = []
+    for N in [100, 200, 400, 800]:
+        grid = oracle.Grid((N,), pad=2, bc_lo=[oracle.BC_PERIODIC], bc_hi=[oracle.BC_PERIODIC],
+                           order=2)
+        U0 = W.smooth_density_wave((N,), vel=[1.0])
+        nsteps = int(math.ceil(1.0 / (0.5 / N / (1.0 + math.sqrt(1.4)))))
+        U = oracle.step(grid, U0, 1.0 / nsteps, nsteps)
+        errs.append(np.sum(np.abs(U[:, 0] - U0[:, 0])) / N)
+    rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    # minmod clips the extrema: L1 rate just under 2 (measured 1.83, 1.85, 1.89)
+    assert np.all(rates >= 1.75) and np.all(rates <= 2.1), rates
+
+
+def test_order2_sod_bounds_and_accuracy():
+    errs = {}
+    for order in (1, 2):
+        for N in (200, 400):
+            grid = oracle.Grid((N,), pad=2, order=order)
+            U, n = oracle.run_cfl(grid, W.sod(N), 0.2)
+            x = (np.arange(N) + 0.5) / N
+            _, Wx = oracle.riemann_exact((1.0, 0.0, 1.0), (0.125, 0.0, 0.1), 1.4,
+                                         (x - 0.5) / 0.2)
+            errs[order, N] = np.sum(np.abs(U[:, 0] - Wx[:, 0])) / N
+            if order == 2:
+                # TVD limiter: no new extrema in the density
+                assert U[:, 0].min() >= 0.125 - 1e-12 and U[:, 0].max() <= 1.0 + 1e-12
+    assert errs[2, 200] < 0.5 * errs[1, 200]
+    rate = math.log2(errs[2, 200] / errs[2, 400])
+    assert 0.7 <= rate <= 1.1, rate
+
+
+@pytest.mark.parametrize("n,bc", [((17,), oracle.BC_TRANSMISSIVE), ((9, 7), oracle.BC_PERIODIC),
+                                  ((5, 6, 4), oracle.BC_REFLECTIVE)])
+def test_order2_uniform_state_bitwise(n, bc):
+    D = len(n)
+    U0 = W.uniform(n, rho=1.3, vel=[0.0] * D, p=0.7)
+    g = oracle.Grid(n, pad=2, bc_lo=[bc] * D, bc_hi=[bc] * D, order=2)
+    assert np.array_equal(oracle.step(g, U0, 0.01, 3), U0)
+
+
+def test_order2_periodic_conservation_and_symmetry():
+    n = (40, 24)
+    per = [oracle.BC_PERIODIC] * 2
+    g = oracle.Grid(n, pad=2, bc_lo=per, bc_hi=per, order=2)
+    U0 = W.random_state(n, seed=11)
+    U = oracle.step(g, U0, 0.2 / 40, 10)
+    tot0, tot = U0.sum(axis=(0, 1)), U.sum(axis=(0, 1))
+    assert np.all(np.abs(tot - tot0) <= 1e-12 * np.abs(U0).sum(axis=(0, 1)))
+    # mirror in x: reverse cells, negate m_x -> the result is the mirrored run
+    N = 60
+    g1 = oracle.Grid((N,), pad=2, order=2)
+    S = W.sod(N)
+    M = S[::-1].copy()
+    M[:, 1] = -M[:, 1]
+    a = oracle.step(g1, S, 0.3 / N, 20)
+    b = oracle.step(g1, M, 0.3 / N, 20)
+    b = b[::-1].copy()
+    b[:, 1] = -b[:, 1]
+    assert np.array_equal(a, b)
+
+
+def test_order2_requires_pad2():
+    with pytest.raises(ValueError):
+        oracle.step(oracle.Grid((16,), pad=1, order=2), W.sod(16), 0.01, 1)
