@@ -49,6 +49,16 @@ WORKLOADS = {
                   label="2-D Euler FORCE 9600x6000 fp64, y-split (paper strong 'large', P:1408)"),
     "pweak": dict(ndim=2, n=(2560, 2500), dtype="f64", scaling="weak",
                   label="2-D Euler FORCE 6.4M cells/GPU fp64, y-split (paper weak, P:1393-1402)"),
+    # order-2 reconstruction (MUSCL-Hancock + FORCE), configs[1] shape
+    "o2_1024": dict(ndim=2, n=(1024, 1024), dtype="f64", scaling="weak", order=2,
+                    label="2-D Euler SLIC (MUSCL-Hancock + FORCE, order 2) 1024x1024/GPU fp64"),
+    # CFL-adaptive steps (Listing 8 wavespeed -> max -> dt every step);
+    # one bench "step" = one run of cfl_steps CFL steps (--cfl-loop device|host)
+    "cfl1024": dict(ndim=2, n=(1024, 1024), dtype="f64", scaling="weak", op="cfl", cfl_steps=20,
+                    label="2-D Euler FORCE 1024x1024/GPU fp64, CFL-adaptive dt (20 steps/run)"),
+    "cfl6400": dict(ndim=2, n=(6400, 4000), dtype="f64", scaling="strong", op="cfl",
+                    cfl_steps=10,
+                    label="2-D Euler FORCE 6400x4000 fp64, CFL-adaptive dt (10 steps/run)"),
 }
 # the paper's Table 4 (sec. 7.3) flux difference, strided layout,
 # one pass over (k*1024)^2 cells; paper V100 times (ms) as context.
@@ -165,7 +175,7 @@ def cpu_baseline(wl, steps_cap=60, budget_s=12.0):
     U = W.shock_bubble(tuple(n), dx=dx)
     if wl["dtype"] == "f32":
         U = U.astype(np.float32)
-    g = oracle.Grid(tuple(n), pad=2, dx=dx)
+    g = oracle.Grid(tuple(n), pad=2, dx=dx, order=wl.get("order", 1))
     dt = 0.4 * dx[0] / oracle.max_wavespeed(g, U.astype(np.float64))
     t0 = time.perf_counter()
     oracle.step(g, U, dt, 1)
@@ -198,7 +208,7 @@ def run_reference(args, wl):
     U = W.shock_bubble(tuple(sample_n), dx=dx)
     if wl["dtype"] == "f32":
         U = U.astype(np.float32)
-    g = oracle.Grid(tuple(sample_n), pad=2, dx=dx)
+    g = oracle.Grid(tuple(sample_n), pad=2, dx=dx, order=wl.get("order", 1))
     dt = 0.4 * dx[0] / oracle.max_wavespeed(g, U.astype(np.float64))
     for _ in range(args.warmup):
         U = oracle.step(g, U, dt, 1)
@@ -232,6 +242,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="2d1024", choices=sorted(WORKLOADS))
+    ap.add_argument("--cfl-loop", default="device", choices=["device", "host"],
+                    help="cfl workloads: rpl_advance_to (device-side dt) or rpl_advance_cfl "
+                         "(host loop: wavespeed pass + sync every step)")
     ap.add_argument("--kernel", default="fused", choices=["fused", "split"])
     ap.add_argument("--dtype", default=None, choices=["f32", "f64"],
                     help="override the workload's dtype (configs[4] runs both)")
@@ -296,7 +309,7 @@ def main():
                    layout=args.layout,
                    nranks=world, rank=rank if world > 1 else 0, nccl_id=nccl_id, device=dev,
                    stream=stream.cuda_stream, rows_per_chunk=args.rows,
-                   transport=args.transport if world > 1 else "nccl")
+                   transport=args.transport if world > 1 else "nccl", order=wl.get("order", 1))
     if world > 1 and args.transport == "p2p":
         blobs = [None] * world
         dist.all_gather_object(blobs, dom.p2p_export())
@@ -331,6 +344,15 @@ def main():
     torch.cuda.synchronize()
 
     launches_per_step = dom.launches_per_step
+    M = wl.get("cfl_steps", 1)
+
+    def run_cfl():
+        # t_end far away: every run takes exactly M steps (the max_steps bound)
+        if args.cfl_loop == "device":
+            t, n = dom.advance_to(1e9, cfl=0.9, n_reduced=0, max_steps=M)
+        else:
+            n = dom.advance_cfl(1e9, cfl=0.9, n_reduced=0, max_steps=M)
+        assert n == M, n
 
     def timed_loop(nsteps, profile):
         """nsteps steps, each bracketed by CUDA events on the library stream, L2
@@ -345,11 +367,14 @@ def main():
         torch.cuda.synchronize()
         # GPU-side head start so the host queues the steps ahead of the GPU:
         # the step events then measure device time, not host launch latency
-        torch.cuda._sleep(200_000 * nsteps)
+        if op != "cfl":  # (a CFL run synchronises inside: it includes its host latency)
+            torch.cuda._sleep(200_000 * nsteps)
         for k in range(nsteps):
             ev[k][0].record(stream)
             if op == "fluxdiff":
                 dom.flux_difference(dt)
+            elif op == "cfl":
+                run_cfl()
             else:
                 dom.advance(dt, 1)
             ev[k][1].record(stream)
@@ -394,6 +419,9 @@ def main():
             if op == "fluxdiff":
                 dom.flux_difference(dt)
                 N_get_fd(dom, h_out.data_ptr())
+            elif op == "cfl":
+                run_cfl()
+                dom.get_state_ptr(h_out.data_ptr())
             else:
                 dom.advance(dt, 1)
                 dom.get_state_ptr(h_out.data_ptr())
@@ -406,17 +434,23 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
         nb = C * local_cells * elem
-        e2e = {"value": global_cells * args.e2e_steps / te / 1e9, "unit": "Gcell-updates/s",
+        e2e = {"value": global_cells * M * args.e2e_steps / te / 1e9, "unit": "Gcell-updates/s",
                "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "steps": args.e2e_steps,
                "path": "rpl_set_state(pinned host) + rpl_advance(dt,1) + rpl_get_state(pinned host)"}
 
-    value = global_cells * args.steps / t_total / 1e9
+    value = global_cells * M * args.steps / t_total / 1e9
+    if op == "cfl":
+        # device loop: M step launches + the initial wavespeed pass; host loop: a
+        # wavespeed pass before every step
+        launches_per_step = M * launches_per_step + (1 if args.cfl_loop == "device" else M)
     if op == "fluxdiff":  # one kernel per call: the step events time the launch
         kern_ms, kern_launches = t_total * 1e3, args.steps
         launches_per_step = 1
     peak, peak_src = measured_peak_gbs()
     alg_bytes = 2 * C * elem * local_cells  # per step-kernel launch (one partition per rank)
     kname = {"fused": {1: "k_sweep", 2: "k_step2d_pt", 3: "k_step3d"}[D], "split": "k_sweep"}[args.kernel]
+    if wl.get("order", 1) == 2:
+        kname = "k_step2d_o2" if (args.kernel == "fused" and D == 2) else "k_sweep2"
     if op == "fluxdiff":
         kname = "k_fluxdiff"
     per_launch_ms = kern_ms / max(kern_launches, 1)
@@ -437,8 +471,8 @@ def main():
     if op == "fluxdiff" and wl.get("paper_ms"):
         # paper Table 4 (V100, strided) time for the same pass: context, other hardware
         vs = wl["paper_ms"] / (t_total / args.steps * 1e3)
-    line = {"metric": "Gcell-updates/s" if op == "step" else "Gcell/s (flux difference)",
-            "value": value, "unit": "Gcell-updates/s" if op == "step" else "Gcell/s",
+    line = {"metric": "Gcell/s (flux difference)" if op == "fluxdiff" else "Gcell-updates/s",
+            "value": value, "unit": "Gcell/s" if op == "fluxdiff" else "Gcell-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True,
             "scaling": wl["scaling"], "vs_baseline": vs, "dtype": wl["dtype"],
@@ -450,6 +484,8 @@ def main():
                              if flush is not None else "not flushed",
                        "timing": "sum of per-step CUDA events on the library stream, max over ranks",
                        "wall_s": wall, "dt": dt, "S0": S0, "op": op,
+                       "cfl": {"loop": args.cfl_loop, "steps_per_run": M, "cfl": 0.9}
+                       if op == "cfl" else None,
                        "paper_v100_ms": wl.get("paper_ms")},
             "roofline": roof, "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary()}

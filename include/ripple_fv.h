@@ -44,7 +44,7 @@ typedef enum {
   RPL_OK = 0,
   RPL_E_INVALID_ARG = -1,
   RPL_E_NOT_DIVISIBLE = -2,  /* size[d] % parts[d] != 0 */
-  RPL_E_PAD_TOO_SMALL = -3,  /* pad < stencil radius r = 1 */
+  RPL_E_PAD_TOO_SMALL = -3,  /* pad < stencil radius (1; 2 for order 2) */
   RPL_E_OOM = -4,
   RPL_E_CUDA = -5,
   RPL_E_NCCL = -6,
@@ -104,10 +104,15 @@ typedef struct {
   int32_t rows_per_chunk;  /* fused kernels: rows (2-D) / planes (3-D) marched per warp task;
                               0 -> automatic */
   rpl_transport transport; /* nranks > 1: NCCL (default) or P2P */
+  int32_t order;           /* reconstruction order (the paper's Listing 8 is
+                              order 1, reading S7): 1 = piecewise constant (default);
+                              2 = MUSCL-Hancock with minmod slopes + FORCE (Toro's SLIC,
+                              DESIGN.md readings F3a-F3d), needs pad >= 2.  Order 2 runs
+                              the fused kernel for 2-D SoA, the split kernel otherwise. */
 } rpl_config;
 
 /* Fill *cfg with defaults: ndim 1, size {1,1,1}, pad 2, parts {1,1,1}, F64, SOA,
- * FUSED, gamma 1.4, dx {1,1,1}, transmissive, nranks 1, device 0. */
+ * FUSED, gamma 1.4, dx {1,1,1}, transmissive, nranks 1, device 0, order 1. */
 void rpl_config_init(rpl_config* cfg);
 
 /* Validate cfg without touching a GPU (host only). */
@@ -159,6 +164,25 @@ rpl_status rpl_max_wavespeed(rpl_domain* dom, double* out);
  * Writes the steps taken to *nsteps_out. */
 rpl_status rpl_advance_cfl(rpl_domain* dom, double t_end, double cfl, int32_t n_reduced,
                            double reduce, int32_t max_steps, int32_t* nsteps_out);
+
+/* Device-side CFL-adaptive advance (the same loop as rpl_advance_cfl,
+ * Listing 8 set_wavespeeds -> reduce(Max) -> set_dt):
+ * S, dt, t and the step count live in device memory.  The initial S is computed
+ * once; afterwards every step kernel folds max |u| + c of the state it writes
+ * into a per-step slot (per-warp max, ordered-bits atomicMax), the slot is
+ * combined over ranks on the stream (P2P: inside the step's flag sync; NCCL: one
+ * 8-byte allreduce MAX), and the next step kernel derives dt = cfl_n min dx / S
+ * (clipped to t_end) itself.  The host only enqueues chunks of steps and reads
+ * (t, n) back once per chunk; kernels launched past t_end exit immediately.
+ * In-kernel |u| + c uses MUFU rsqrt/rcp + Newton (within a few ulp of
+ * rpl_max_wavespeed's IEEE formula), so dt may differ from rpl_advance_cfl's
+ * in the last bits (reading "device CFL").  Writes the time reached
+ * (t_end unless max_steps ran out) and the steps taken; either pointer may be
+ * NULL.  Collective; synchronises once per chunk.  Errors: RPL_E_INVALID_ARG
+ * (cfl <= 0, t_end < 0, max_steps < 0, a 2-D RPL_VARIANT without the device
+ * step), RPL_E_DOMAIN (rho <= 0, p <= 0, non-finite state or S <= 0). */
+rpl_status rpl_advance_to(rpl_domain* dom, double t_end, double cfl, int32_t n_reduced,
+                          double reduce, int32_t max_steps, double* t_out, int32_t* nsteps_out);
 
 /* Wait for all enqueued work; report deferred RPL_E_DOMAIN / CUDA / NCCL errors. */
 rpl_status rpl_synchronize(rpl_domain* dom);

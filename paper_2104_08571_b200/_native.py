@@ -31,7 +31,8 @@ class Config(ctypes.Structure):
                 ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("nccl_id", ctypes.c_void_p), ("device", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("arena", ctypes.c_void_p),
-                ("rows_per_chunk", ctypes.c_int32), ("transport", ctypes.c_int)]
+                ("rows_per_chunk", ctypes.c_int32), ("transport", ctypes.c_int),
+                ("order", ctypes.c_int32)]
 
 
 class HaloEdge(ctypes.Structure):
@@ -44,6 +45,7 @@ class HaloEdge(ctypes.Structure):
 EXPORTS = ["rpl_config_init", "rpl_config_check", "rpl_arena_bytes", "rpl_nccl_unique_id",
            "rpl_create", "rpl_local_box", "rpl_set_state", "rpl_get_state", "rpl_get_padded",
            "rpl_fill_padding", "rpl_advance", "rpl_max_wavespeed", "rpl_advance_cfl",
+           "rpl_advance_to",
            "rpl_synchronize", "rpl_launches_per_step", "rpl_profile", "rpl_profile_read",
            "rpl_halo_plan", "rpl_p2p_export", "rpl_p2p_attach",
            "rpl_flux_difference", "rpl_get_flux_difference", "rpl_destroy",
@@ -78,6 +80,9 @@ def lib():
     L.rpl_max_wavespeed.argtypes = [vp, P(ctypes.c_double)]
     L.rpl_advance_cfl.argtypes = [vp, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
                                   ctypes.c_double, ctypes.c_int32, P(ctypes.c_int32)]
+    L.rpl_advance_to.argtypes = [vp, ctypes.c_double, ctypes.c_double, ctypes.c_int32,
+                                 ctypes.c_double, ctypes.c_int32, P(ctypes.c_double),
+                                 P(ctypes.c_int32)]
     L.rpl_synchronize.argtypes = [vp]
     L.rpl_launches_per_step.argtypes = [vp, P(ctypes.c_int32)]
     L.rpl_profile.argtypes = [vp, ctypes.c_int32]

@@ -66,6 +66,11 @@ __global__ void __launch_bounds__(256) k_sweep(const __grid_constant__ KArgs<T> 
   constexpr int C = D + 2;
   const Geom& g = a.g;
   const int64_t n = g.cells();
+  Coef<T> k;
+  if (!step_coef(a, k)) return;
+  const bool ws = a.cf.dev != nullptr && a.cf.last;
+  const T gam = (T)a.cf.gamma;
+  T wmax = T(0);
   int bad = 0, nan = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -81,15 +86,61 @@ __global__ void __launch_bounds__(256) k_sweep(const __grid_constant__ KArgs<T> 
     bad |= phys_flux<D, d>(U0, F0, a.gm1);
     phys_flux<D, d>(Up, Fp, a.gm1);
     T PL[C], PR[C], o[C];
-    force_face<D, d>(Um, Fm, U0, F0, PL, a.q[d], a.nq2[d], a.gm1);
-    force_face<D, d>(U0, F0, Up, Fp, PR, a.q[d], a.nq2[d], a.gm1);
+    force_face<D, d>(Um, Fm, U0, F0, PL, k.q[d], k.nq2[d], a.gm1);
+    force_face<D, d>(U0, F0, Up, Fp, PR, k.q[d], k.nq2[d], a.gm1);
 #pragma unroll
     for (int c = 0; c < C; ++c) o[c] = U0[c] - (PR[c] - PL[c]);
     nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
     store_cell<D, L>(g, a.out, x, y, z, o);
+    if (ws) wmax = fmax(wmax, wavespeed<D>(o, a.gm1, gam));
     if (near_face<D>(g, x, y, z)) images<D, L>(a, x, y, z, o);
   }
   if (bad < 0 || nan >= kExpMask<T>) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
+}
+
+// ---------------------------------------------------------------------------
+// K-A, order 2: one sweep along d with MUSCL-Hancock + FORCE.  Thread
+// per interior cell: loads U_{i-2..i+2}, evolves the boundary values of cells
+// i-1, i, i+1 (hancock), FORCE at faces i-1/2 and i+1/2, update.
+// ---------------------------------------------------------------------------
+template <typename T, int D, int d, int L>
+__global__ void __launch_bounds__(256) k_sweep2(const __grid_constant__ KArgs<T> a) {
+  constexpr int C = D + 2;
+  const Geom& g = a.g;
+  const int64_t n = g.cells();
+  Coef<T> k;
+  if (!step_coef(a, k)) return;
+  const bool ws = a.cf.dev != nullptr && a.cf.last;
+  const T gam = (T)a.cf.gamma;
+  T wmax = T(0);
+  int bad = 0, nan = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = i % g.S[0];
+    const int64_t y = (i / g.S[0]) % g.S[1];
+    const int64_t z = i / (g.S[0] * g.S[1]);
+    const int64_t dm[3] = {d == 0 ? 1 : 0, d == 1 ? 1 : 0, d == 2 ? 1 : 0};
+    T U[5][C];
+#pragma unroll
+    for (int j = 0; j < 5; ++j)
+      load_cell<D, L>(g, a.in, x + (j - 2) * dm[0], y + (j - 2) * dm[1], z + (j - 2) * dm[2], U[j]);
+    T bL[3][C], FbL[3][C], bR[3][C], FbR[3][C];
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      bad |= hancock<D, d>(U[j], U[j + 1], U[j + 2], k.h2[d], a.gm1, bL[j], FbL[j], bR[j], FbR[j]);
+    T PL[C], PR[C], o[C];
+    force_face<D, d>(bR[0], FbR[0], bL[1], FbL[1], PL, k.q[d], k.nq2[d], a.gm1);
+    force_face<D, d>(bR[1], FbR[1], bL[2], FbL[2], PR, k.q[d], k.nq2[d], a.gm1);
+#pragma unroll
+    for (int c = 0; c < C; ++c) o[c] = U[2][c] - (PR[c] - PL[c]);
+    nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
+    store_cell<D, L>(g, a.out, x, y, z, o);
+    if (ws) wmax = fmax(wmax, wavespeed<D>(o, a.gm1, gam));
+    if (near_face<D>(g, x, y, z)) images<D, L>(a, x, y, z, o);
+  }
+  if (bad < 0 || nan >= kExpMask<T>) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
 }
 
 // ---------------------------------------------------------------------------
@@ -545,7 +596,12 @@ __global__ void __launch_bounds__(32 * NW, MB)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int SX = (int)g.S[0], SY = (int)g.S[1];
   const int G = gridDim.x;
-  const T gm1 = a.gm1, qx = a.q[0], nqx = a.nq2[0], qy = a.q[1], nqy = a.nq2[1];
+  Coef<T> kc;
+  if (!step_coef(a, kc)) return;
+  const bool ws = a.cf.dev != nullptr;
+  const T gam = (T)a.cf.gamma;
+  T wmax = T(0);
+  const T gm1 = a.gm1, qx = kc.q[0], nqx = kc.nq2[0], qy = kc.q[1], nqy = kc.nq2[1];
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -731,6 +787,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
       for (int v = 0; v < V; ++v) {
         if (ok[v]) {
           nan = max(nan, max(naninf(o[v][0]), naninf(o[v][C - 1])));
+          if (ws) wmax = fmax(wmax, wavespeed<D>(o[v], gm1, gam));
           const int xv = xw + V * lane + v;
           if (yface | (xv < g.pad) | (xv >= SX - g.pad)) images<D, 0>(a, xv, yr, 0, o[v]);
         }
@@ -738,6 +795,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
     }
   }
   if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
 }
 
 template <typename T, int V, int NW, int MB = (V == 1 ? 2 : 1)>
@@ -763,6 +821,232 @@ static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   if (grid > ntiles) grid = ntiles;
   k_step2d_pt<T, V, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
+}
+
+// ---------------------------------------------------------------------------
+// K-B (2-D), order 2: MUSCL-Hancock + FORCE, both sweeps of a step
+// in one HBM pass.  Persistent CTAs of NW warps; a tile is 28 x-cells x (NW-4)
+// rows (stencil radius 2 in both directions), TMA streams the tiles' [NW rows]
+// [C][32+AL] input boxes into a 2-stage ring.  Per tile, warp j owns row
+// yr = y0 - 2 + j:
+//   X   lane = x slot: slopes from shuffled neighbours, evolved boundary values
+//       (hancock), face l+1/2 = FORCE(Ubar^R_l, Ubar^L_{l+1}) (shuffle), update
+//       -> U* (valid on slots 2..29), published to shared memory;
+//   Y1  rows 1..NW-2: y-slopes from the rows above/below, evolved y boundary
+//       values; Ubar^R and F_y(Ubar^R) published;
+//   Y2  rows 2..NW-2: y-face between rows j-1 and j, published;
+//   upd rows 2..NW-3: U^{n+1} = U* - (Phi_{j+1/2} - Phi_{j-1/2}), store + images.
+// ---------------------------------------------------------------------------
+template <typename T, int NW>
+struct SmemO2 {
+  static constexpr int W = 32, C = 4;
+  static constexpr int AL = 16 / (int)sizeof(T);
+  static constexpr int WB = W + AL;
+  static constexpr int STAGE = NW * C * WB;
+  static constexpr int SX = NW * C * W;
+  static constexpr int BR = NW * 2 * C * W;
+  static constexpr int FY = NW * C * W;
+  static constexpr size_t bytes() { return (size_t)(2 * STAGE + SX + BR + FY) * sizeof(T) + 64; }
+};
+
+template <typename T, int NW, int MB>
+__global__ void __launch_bounds__(32 * NW, MB)
+    k_step2d_o2(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
+                int nwin, int ntiles) {
+  constexpr int D = 2, C = 4, W = 32;
+  using SM = SmemO2<T, NW>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  T* stage = reinterpret_cast<T*>(smem);
+  T* sx = stage + 2 * SM::STAGE;
+  T* br = sx + SM::SX;
+  T* fyb = br + SM::BR;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + SM::FY);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int SX = (int)g.S[0], SY = (int)g.S[1];
+  const int G = gridDim.x;
+  Coef<T> kc;
+  if (!step_coef(a, kc)) return;
+  const bool ws = a.cf.dev != nullptr;
+  const T gam = (T)a.cf.gamma;
+  T wmax = T(0);
+  const T gm1 = a.gm1;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int i) {
+    const int tile = blockIdx.x + i * G;
+    if (tile >= ntiles) return;
+    const int s = i & 1;
+    const int w = tile % nwin, yb = tile / nwin;
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
+    const int x0 = (int)g.xo + w * (W - 4) - 2;
+    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
+                 (int)g.off[1] + yb * (NW - 4) - 2, 0);
+  };
+  if (threadIdx.x == 0) {
+    issue(0);
+    issue(1);
+  }
+  int bad = 0, nan = 0;
+  const bool lane_in = (lane >= 1) & (lane <= 30);   // has both x-neighbours
+  const bool lane_out = (lane >= 2) & (lane <= 29);  // U* valid
+  for (int i = 0;; ++i) {
+    const int tile = blockIdx.x + i * G;
+    if (tile >= ntiles) break;
+    const int win = tile % nwin, yb = tile / nwin;
+    const int xw = win * (W - 4) - 2;
+    const int yr = yb * (NW - 4) - 2 + warp;
+    const int xv = xw + lane;
+    const bool row_in = yr <= SY + 1;
+    const int s = i & 1;
+    mbar_wait(&bar[s], (i >> 1) & 1);
+    // ---- X
+    T S_[C];
+    {
+      T U[C], Um[C], Up[C];
+      const int sh = ((int)g.xo + xw) % SM::AL;
+      const T* st = stage + s * SM::STAGE + warp * C * SM::WB + sh + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) U[c] = st[c * SM::WB];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Um[c] = __shfl_up_sync(kFull, U[c], 1);
+        Up[c] = __shfl_down_sync(kFull, U[c], 1);
+      }
+      T bL[C], FbL[C], bR[C], FbR[C];
+      const int b = hancock<D, 0>(Um, U, Up, kc.h2[0], gm1, bL, FbL, bR, FbR);
+      bad |= (lane_in & (xv >= -1) & (xv <= SX) & row_in) ? b : 0;
+      T Pnx[C];
+      {
+        T bLn[C], FbLn[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          bLn[c] = __shfl_down_sync(kFull, bL[c], 1);
+          FbLn[c] = __shfl_down_sync(kFull, FbL[c], 1);
+        }
+        force_face<D, 0>(bR, FbR, bLn, FbLn, Pnx, kc.q[0], kc.nq2[0], gm1);
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const T Ppv = __shfl_up_sync(kFull, Pnx[c], 1);
+        S_[c] = U[c] - (Pnx[c] - Ppv);
+      }
+      T* xr = sx + warp * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) xr[c * W] = S_[c];
+    }
+    __syncthreads();  // (A) stage s consumed; U* published
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      issue(i + 2);
+    }
+    // ---- Y1: evolved y boundary values of this row
+    T byL[C], FbyL[C];
+    if (warp >= 1 && warp <= NW - 2) {
+      T Sm[C], Sp[C], byR[C], FbyR[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Sm[c] = sx[(warp - 1) * C * W + c * W + lane];
+        Sp[c] = sx[(warp + 1) * C * W + c * W + lane];
+      }
+      const int b = hancock<D, 1>(Sm, S_, Sp, kc.h2[1], gm1, byL, FbyL, byR, FbyR);
+      bad |= (lane_out & (xv < SX) & (yr >= -1) & (yr <= SY)) ? b : 0;
+      T* w = br + warp * 2 * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        w[c * W] = byR[c];
+        w[(C + c) * W] = FbyR[c];
+      }
+    }
+    __syncthreads();  // (B) Ubar^R_y published
+    // ---- Y2: face between rows warp-1 and warp
+    T Py[C];
+    if (warp >= 2 && warp <= NW - 2) {
+      T pR[C], pF[C];
+      const T* r = br + (warp - 1) * 2 * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        pR[c] = r[c * W];
+        pF[c] = r[(C + c) * W];
+      }
+      force_face<D, 1>(pR, pF, byL, FbyL, Py, kc.q[1], kc.nq2[1], gm1);
+      T* fw = fyb + warp * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) fw[c * W] = Py[c];
+    }
+    __syncthreads();  // (C) y-faces published
+    // ---- update + store
+    if (warp >= 2 && warp <= NW - 3 && yr < SY && lane_out && xv < SX) {
+      const T* fu = fyb + (warp + 1) * C * W + lane;
+      T o[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) o[c] = S_[c] - (fu[c * W] - Py[c]);
+      T* dst = a.out + g.row(yr, 0) * g.rstride + g.xo + xv;
+#pragma unroll
+      for (int c = 0; c < C; ++c) dst[c * g.cstride] = o[c];
+      nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
+      if (ws) wmax = fmax(wmax, wavespeed<D>(o, gm1, gam));
+      if ((yr < g.pad) | (yr >= SY - g.pad) | (xv < g.pad) | (xv >= SX - g.pad))
+        images<D, 0>(a, xv, yr, 0, o);
+    }
+  }
+  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
+}
+
+template <typename T, int NW, int MB>
+static void launch_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  constexpr int W = 32;
+  using SM = SmemO2<T, NW>;
+  const int nwin = (int)((a.g.S[0] + (W - 4) - 1) / (W - 4));
+  const int nyb = (int)((a.g.S[1] + (NW - 4) - 1) / (NW - 4));
+  const int ntiles = nwin * nyb;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(k_step2d_o2<T, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SM::bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step2d_o2<T, NW, MB>, 32 * NW,
+                                                  SM::bytes());
+    if (per_sm < 1) per_sm = 1;
+  }
+  int nsm = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int grid = per_sm * nsm;
+  if (grid > ntiles) grid = ntiles;
+  k_step2d_o2<T, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
+}
+
+// order-2 variants (RPL_VARIANT; box rows = NW)
+static int o2_rows(int variant) {
+  switch (variant) {
+    case 71: return 12;
+    case 72: return 12;
+    case 73: return 24;
+    default: return 16;
+  }
+}
+
+int tmap2d_box_o2(const Geom& g, int variant, int* box_w, int* box_rows) {
+  *box_w = 32 + 16 / g.elem;
+  *box_rows = o2_rows(variant);
+  return 1;
+}
+
+template <typename T>
+static void launch_step2d_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  switch (a.variant) {
+    case 71: return launch_o2<T, 12, 2>(a, tmap, s);
+    case 72: return launch_o2<T, 12, 1>(a, tmap, s);
+    case 73: return launch_o2<T, 24, 1>(a, tmap, s);
+    default: return launch_o2<T, 16, 1>(a, tmap, s);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1402,6 +1686,9 @@ int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
     case 36: *box_w = 64 + al; *box_rows = 8; return 1;
     case 37: case 39: *box_w = 32 + al; *box_rows = 12; return 1;
     case 38: *box_w = 32 + al; *box_rows = 10; return 1;
+    case 44: *box_w = 32 + al; *box_rows = 24; return 1;
+    case 46: *box_w = 32 + al; *box_rows = 14; return 1;
+    case 47: *box_w = 32 + al; *box_rows = 20; return 1;
     case 40: case 41: *box_w = 32 + al; *box_rows = 8; return 1;
     case 42: *box_w = 64 + al; *box_rows = 8; return 1;
     case 43: *box_w = 32 + al; *box_rows = 16; return 1;
@@ -1519,6 +1806,14 @@ static int grid_for(int64_t n, int block) {
 template <typename T, int D, int L>
 static void sweep_dispatch_d(const KArgs<T>& a, int d, cudaStream_t s) {
   const int grid = grid_for(a.g.cells(), 256);
+  if (a.order == 2) {
+    if (d == 0) k_sweep2<T, D, 0, L><<<grid, 256, 0, s>>>(a);
+    if constexpr (D > 1)
+      if (d == 1) k_sweep2<T, D, 1, L><<<grid, 256, 0, s>>>(a);
+    if constexpr (D > 2)
+      if (d == 2) k_sweep2<T, D, 2, L><<<grid, 256, 0, s>>>(a);
+    return;
+  }
   if (d == 0) k_sweep<T, D, 0, L><<<grid, 256, 0, s>>>(a);
   if constexpr (D > 1)
     if (d == 1) k_sweep<T, D, 1, L><<<grid, 256, 0, s>>>(a);
@@ -1557,6 +1852,7 @@ int auto_rows_3d(const Geom& g) {
 
 template <typename T>
 void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  if (a.order == 2) return launch_step2d_o2<T>(a, tmap, s);
   switch (a.variant) {
     case 30: return launch_pt2d<T, 1, 16>(a, tmap, s);
     case 31: return launch_pt2d<T, 2, 8>(a, tmap, s);
@@ -1576,6 +1872,9 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 37: return launch_pt2d<T, 1, 12, 2>(a, tmap, s);
     case 38: return launch_pt2d<T, 1, 10, 3>(a, tmap, s);
     case 39: return launch_pt2d<T, 1, 12, 3>(a, tmap, s);
+    case 44: return launch_pt2d<T, 1, 24, 1>(a, tmap, s);
+    case 46: return launch_pt2d<T, 1, 14, 2>(a, tmap, s);
+    case 47: return launch_pt2d<T, 1, 20, 1>(a, tmap, s);
     default: break;
   }
   KArgs<T> am = a;

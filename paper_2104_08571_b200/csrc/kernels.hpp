@@ -18,7 +18,8 @@ int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s);  // K-B 
 int make_tmap3d(const Geom& g, const void* buf, void* map_out, int variant);
 // 4-D tensor map {pitch, C, P1, P2} of a SoA buffer with box {box_w, C, box_rows, 1}
 int make_tmap(const Geom& g, const void* buf, void* map_out, int box_w, int box_rows);
-int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows);  // 0 if 2-D uses TMA  // 128-byte CUtensorMap
+int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows);
+int tmap2d_box_o2(const Geom& g, int variant, int* box_w, int* box_rows);  // order-2 kernel  // 0 if 2-D uses TMA  // 128-byte CUtensorMap
 int window3d(const Geom& g);                                     // outputs per 3-D x-window
 template <typename T>
 void launch_fill(const Geom& g, int part, T* const* bufs, cudaStream_t s);
@@ -28,6 +29,10 @@ void launch_maxws(const Geom& g, const T* in, double gamma, unsigned long long* 
 
 template <typename T>
 void launch_fluxdiff(const KArgs<T>& a, cudaStream_t s);  // sec. 7.3 flux difference (f2)
+
+// 2-D variants whose kernel implements the device-side CFL step (k_step2d_pt)
+inline bool step2d_has_cfl(int variant) { return variant == 0 || (variant >= 30 && variant <= 39) || variant == 44 || variant == 46 ||
+         variant == 47; }
 
 int auto_rows_2d(const Geom& g);
 int auto_rows_3d(const Geom& g);

@@ -104,6 +104,11 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
   const bool row_out = (warp >= 1) & (warp <= TY) & (yr < SY);
   const bool yface = (yr < g.pad) | (yr >= SY - g.pad);
   const T gm1 = a.gm1;
+  Coef<T> kc;
+  if (!step_coef(a, kc)) return;
+  const bool ws = a.cf.dev != nullptr;
+  const T gam = (T)a.cf.gamma;
+  T wmax = T(0);
 
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -128,7 +133,7 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
 
   ZState<T, V> zs;
   int bad = 0, nan = 0;
-  const T qx = a.q[0], nqx = a.nq2[0], qy = a.q[1], nqy = a.nq2[1], qz = a.q[2], nqz = a.nq2[2];
+  const T qx = kc.q[0], nqx = kc.nq2[0], qy = kc.q[1], nqy = kc.nq2[1], qz = kc.q[2], nqz = kc.nq2[2];
   T* dst_row = a.out + g.row(yr, z0 - 1) * g.rstride + (g.xo + xw + V * lane) * g.xstride;
   const int64_t plane = g.rstride * g.P[1];
 
@@ -238,6 +243,7 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
           for (int v = 0; v < V; ++v) {
             if (out_ok[v] & row_out) {
               nan = max(nan, max(naninf(o[v][0]), naninf(o[v][C - 1])));
+              if (ws) wmax = fmax(wmax, wavespeed<D>(o[v], gm1, gam));
 #pragma unroll
               for (int c = 0; c < C; ++c) dp[c * g.cstride + v * g.xstride] = o[v][c];
               const bool zf = (z - 1 < g.pad) | (z - 1 >= SZ - g.pad);
@@ -266,6 +272,7 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
     }
   }
   if (__any_sync(0xffffffffu, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
 }
 
 // ------------------------------------------------------------------ host side

@@ -11,6 +11,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -231,12 +232,17 @@ struct rpl_domain {
   TMap tmap[2][kMaxParts];
   bool tmaps_ok = false;
   // P2P transport
-  unsigned long long* ctl = nullptr;        // [0,64): step flags from each rank, [64,128): max slots
+  unsigned long long* ctl = nullptr;        // [0,64): step flags from each rank, then 4 sets of
+                                            // [64] wavespeed slots (set 0: rpl_max_wavespeed,
+                                            // sets 1-3: device CFL, rotated by step)
   int64_t base_off = 0;                     // arena -> 256-aligned buffer base
   bool p2p = false, p2p_attached = false;
   void* peer_arena[kMaxParts] = {nullptr};  // IPC mappings (to close)
   unsigned long long** d_peer_ctl = nullptr;  // device [nranks]: each rank's control block
-  unsigned long long epoch = 0;  // RPL_VARIANT env: fused-kernel occupancy variant (tuning)
+  unsigned long long epoch = 0;
+  // device-side CFL (rpl_advance_to)
+  CflDev* d_cfl = nullptr;
+  CflDev* h_cfl = nullptr;  // pinned
   // kernel timing (rpl_profile)
   std::vector<cudaEvent_t> ev;  // pairs
   size_t ev_used = 0;
@@ -244,8 +250,8 @@ struct rpl_domain {
 
 static int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
-// control block after the buffers: P2P step flags [64] and wavespeed slots [64]
-constexpr int64_t kCtlBytes = 2 * kMaxParts * 8;
+// control block after the buffers: P2P step flags [64] and 4 x wavespeed slots [64]
+constexpr int64_t kCtlBytes = 5 * kMaxParts * 8;
 
 extern "C" void rpl_config_init(rpl_config* c) {
   memset(c, 0, sizeof(*c));
@@ -259,6 +265,7 @@ extern "C" void rpl_config_init(rpl_config* c) {
   c->gamma = 1.4;
   c->dx[0] = c->dx[1] = c->dx[2] = 1.0;
   c->nranks = 1;
+  c->order = 1;
 }
 
 static rpl_status geom_of(const rpl_config* c, Geom* g) {
@@ -289,6 +296,9 @@ static rpl_status geom_of(const rpl_config* c, Geom* g) {
   if (c->transport == RPL_TRANSPORT_P2P && c->nranks > 1 && c->arena)
     return fail(RPL_E_INVALID_ARG, "P2P transport needs a library-owned arena (CUDA IPC)");
   if (c->rows_per_chunk < 0) return fail(RPL_E_INVALID_ARG, "rows_per_chunk must be >= 0");
+  if (c->order != 1 && c->order != 2) return fail(RPL_E_INVALID_ARG, "order must be 1 or 2");
+  if (c->order == 2 && c->pad < 2)
+    return fail(RPL_E_PAD_TOO_SMALL, "order 2 (MUSCL-Hancock) needs pad >= 2 (stencil radius 2)");
   return RPL_OK;
 }
 
@@ -352,6 +362,8 @@ static void free_domain(rpl_domain* d) {
   if (d->d_tab) cudaFree(d->d_tab);
   if (d->d_flag) cudaFree(d->d_flag);
   if (d->d_smax) cudaFree(d->d_smax);
+  if (d->d_cfl) cudaFree(d->d_cfl);
+  if (d->h_cfl) cudaFreeHost(d->h_cfl);
   if (d->h_flag) cudaFreeHost(d->h_flag);
   if (d->h_smax) cudaFreeHost(d->h_smax);
   if (d->stage) cudaFree(d->stage);
@@ -401,6 +413,8 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
   CU(cudaMemsetAsync(d->d_flag, 0, sizeof(unsigned), d->stream));
   CU(cudaMallocHost(&d->h_flag, sizeof(unsigned)));
   CU(cudaMallocHost(&d->h_smax, sizeof(unsigned long long)));
+  CU(cudaMalloc(&d->d_cfl, sizeof(CflDev)));
+  CU(cudaMallocHost(&d->h_cfl, sizeof(CflDev)));
   if (const char* v = getenv("RPL_VARIANT")) d->variant = atoi(v);
   if (g.D == 3) {  // SoA and AoS
     d->tmaps_ok = true;
@@ -414,7 +428,9 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
   }
   {
     int bw = 0, br = 0;
-    if (g.D == 2 && g.layout == 0 && tmap2d_box(g, d->variant, &bw, &br)) {
+    const bool box = c->order == 2 ? tmap2d_box_o2(g, d->variant, &bw, &br)
+                                   : tmap2d_box(g, d->variant, &bw, &br);
+    if (g.D == 2 && g.layout == 0 && box) {
       for (int p : d->local)
         for (int b = 0; b < 2; ++b)
           if (make_tmap(g, d->buf[b][p], d->tmap[b][p].b, bw, br) != 0)
@@ -663,17 +679,20 @@ static rpl_status exchange_t(rpl_domain* d, int b) {
 // P2P: one warp publishes "rank `me` finished epoch e" into every peer's control
 // block (system-scope release after a system fence, so the step kernel's peer
 // stores are visible first) and waits until every peer published e (acquire).
-// With mode 1 it also publishes the local wavespeed max into the peers' slots
-// and reduces the slots afterwards (exact: max).
+// With mode 1 it also publishes the local wavespeed max *smax into slot `me` of
+// the peers' slot set `set` and, after the wait, reduces its own set into *smax
+// (exact: max).  Sets rotate with the step (device CFL): a rank is at most one
+// epoch ahead of any peer, so a set is never rewritten before it was read.
 __global__ void k_p2p_sync(unsigned long long* const* ctl, int me, int nranks,
-                           unsigned long long epoch, unsigned long long* smax, int mode) {
+                           unsigned long long epoch, unsigned long long* smax, int set, int mode) {
   const int r = threadIdx.x;
   unsigned long long* mine = ctl[me];
+  const int so = kMaxParts * (1 + set);
   if (r < nranks && r != me) {
     unsigned long long* peer = ctl[r];
     if (mode == 1) {
       const unsigned long long v = *smax;
-      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(peer + kMaxParts + me), "l"(v)
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(peer + so + me), "l"(v)
                    : "memory");
     }
     __threadfence_system();
@@ -690,7 +709,7 @@ __global__ void k_p2p_sync(unsigned long long* const* ctl, int me, int nranks,
     for (int q = 0; q < nranks; ++q)
       if (q != me) {
         unsigned long long v;
-        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + kMaxParts + q)
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + so + q)
                      : "memory");
         m = v > m ? v : m;
       }
@@ -698,12 +717,21 @@ __global__ void k_p2p_sync(unsigned long long* const* ctl, int me, int nranks,
   }
 }
 
-static rpl_status p2p_sync(rpl_domain* d, int mode) {
+static rpl_status p2p_sync(rpl_domain* d, int mode, unsigned long long* smax = nullptr,
+                           int set = 0) {
   if (!d->p2p_attached) return fail(RPL_E_INVALID_ARG, "P2P transport: call rpl_p2p_attach first");
   ++d->epoch;
   k_p2p_sync<<<1, 32, 0, d->stream>>>(d->d_peer_ctl, d->cfg.rank, d->cfg.nranks, d->epoch,
-                                      d->d_smax, mode);
+                                      smax ? smax : d->d_smax, set, mode);
   CU(cudaGetLastError());
+  return RPL_OK;
+}
+
+// Combine the ranks' wavespeed slot (max) on the stream; no-op for one rank.
+static rpl_status reduce_max(rpl_domain* d, unsigned long long* slot, int set) {
+  if (d->cfg.nranks <= 1) return RPL_OK;
+  if (d->p2p) return p2p_sync(d, 1, slot, set);
+  NC(g_nccl.AllReduce(slot, slot, 1, ncclUint64, ncclMax, d->comm, d->stream));
   return RPL_OK;
 }
 
@@ -736,6 +764,8 @@ extern "C" rpl_status rpl_fill_padding(rpl_domain* d) {
 }
 
 static bool use_fused(const rpl_domain* d) {
+  if (d->cfg.order == 2)  // order 2: fused 2-D SoA kernel; 3-D and AoS run the split kernel
+    return d->cfg.kernel == RPL_KERNEL_FUSED && d->g.D == 2 && d->g.layout == 0;
   return d->cfg.kernel == RPL_KERNEL_FUSED &&
          ((d->g.D == 2 && d->g.layout == 0) || (d->g.D == 3 && d->tmaps_ok));
 }
@@ -752,8 +782,11 @@ extern "C" rpl_status rpl_launches_per_step(const rpl_domain* d, int32_t* out) {
   return RPL_OK;
 }
 
+// Enqueue nsteps steps.  cf == nullptr: fixed dt.  Otherwise device-side CFL
+// steps cf->step .. cf->step + nsteps - 1 (dt derived on the device, see
+// scheme.cuh step_coef); after each step the ranks' wavespeed slot is combined.
 template <typename T>
-static rpl_status advance_t(rpl_domain* d, double dt, int nsteps) {
+static rpl_status advance_t(rpl_domain* d, double dt, int nsteps, const CflArgs* cf = nullptr) {
   const Geom& g = d->g;
   KArgs<T> a;
   memset(&a, 0, sizeof(a));
@@ -762,16 +795,21 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps) {
     const double lam = k < g.D ? dt / d->cfg.dx[k] : 0.0;
     a.q[k] = (T)(0.25 * lam);
     a.nq2[k] = (T)(-0.25 * lam * lam);
+    a.h2[k] = (T)(0.5 * lam);
   }
   a.gm1 = (T)(d->cfg.gamma - 1.0);
   a.flag = d->d_flag;
   a.rows = d->rows;
   a.variant = d->variant;
+  a.order = d->cfg.order;
+  if (cf) a.cf = *cf;
   const bool fused = use_fused(d);
   for (int s = 0; s < nsteps; ++s) {
     const int nsweep = fused ? 1 : g.D;
+    if (cf) a.cf.step = cf->step + s;
     for (int sw = 0; sw < nsweep; ++sw) {
       const int nb = d->cur ^ 1;
+      a.cf.last = sw == nsweep - 1;
       a.outs = (T* const*)(d->d_tab + nb * kMaxParts);
       for (int p : d->local) {
         a.part = p;
@@ -790,7 +828,18 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps) {
         }
       }
       CU(cudaGetLastError());
-      rpl_status st = exchange(d, nb);
+      rpl_status st;
+      if (cf && a.cf.last && d->cfg.nranks > 1) {
+        const int sn = (a.cf.step + 1) % 3;
+        if (d->p2p) {
+          st = p2p_sync(d, 1, &cf->dev->S[sn], 1 + sn);  // halo epoch + wavespeed in one sync
+        } else {
+          st = exchange(d, nb);
+          if (!st) st = reduce_max(d, &cf->dev->S[sn], 0);
+        }
+      } else {
+        st = exchange(d, nb);
+      }
       if (st) return st;
       d->cur = nb;  // Listing 8 swap: the current state is the last-written buffer
     }
@@ -822,11 +871,9 @@ extern "C" rpl_status rpl_max_wavespeed(rpl_domain* d, double* out) {
                           d->d_flag, d->stream);
   }
   CU(cudaGetLastError());
-  if (d->cfg.nranks > 1 && d->p2p) {
-    rpl_status st = p2p_sync(d, 1);
+  {
+    rpl_status st = reduce_max(d, d->d_smax, 0);
     if (st) return st;
-  } else if (d->cfg.nranks > 1) {
-    NC(g_nccl.AllReduce(d->d_smax, d->d_smax, 1, ncclUint64, ncclMax, d->comm, d->stream));
   }
   CU(cudaMemcpyAsync(d->h_smax, d->d_smax, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                      d->stream));
@@ -868,6 +915,91 @@ extern "C" rpl_status rpl_advance_cfl(rpl_domain* d, double t_end, double cfl, i
   if (nsteps_out) *nsteps_out = n;
   if (st) return st;
   return rpl_synchronize(d);
+}
+
+// Device-side CFL run.  Same loop as rpl_advance_cfl, but S, dt, t
+// and n live on the device: the initial S comes from k_maxws, each step kernel
+// folds max |u| + c of the state it produces into the next slot, the slot is
+// combined across ranks on the stream, and every step kernel derives its dt
+// from it.  The host enqueues chunks of steps (kernels past t_end exit at once)
+// and reads (t, n) back once per chunk.
+template <typename T>
+static rpl_status advance_to_t(rpl_domain* d, const CflArgs& base, int max_steps, double* t_out,
+                               int32_t* n_out) {
+  CflDev init;
+  memset(&init, 0, sizeof(init));
+  CU(cudaMemcpyAsync(d->d_cfl, &init, sizeof(init), cudaMemcpyHostToDevice, d->stream));
+  for (int p : d->local)
+    launch_maxws<T>(d->g, (const T*)d->buf[d->cur][p], d->cfg.gamma, &d->d_cfl->S[0], d->d_flag,
+                    d->stream);
+  CU(cudaGetLastError());
+  rpl_status st = reduce_max(d, &d->d_cfl->S[0], 1);
+  if (st) return st;
+  const int nsweep = use_fused(d) ? 1 : d->g.D;
+  const int cur0 = d->cur;
+  int launched = 0, chunk = 8;
+  double t_prev = 0.0;
+  int n_prev = 0;
+  if (const char* v = getenv("RPL_CFL_CHUNK")) chunk = atoi(v) > 0 ? atoi(v) : chunk;
+  int n = 0;
+  double t = 0.0;
+  while (launched < max_steps) {
+    const int k = std::min(chunk, max_steps - launched);
+    CflArgs cf = base;
+    cf.step = launched;
+    st = advance_t<T>(d, 0.0, k, &cf);
+    if (st) return st;
+    launched += k;
+    CU(cudaMemcpyAsync(d->h_cfl, d->d_cfl, sizeof(CflDev), cudaMemcpyDeviceToHost, d->stream));
+    st = check_flag(d);  // synchronises the stream
+    n = d->h_cfl->n;
+    t = d->h_cfl->t[n & 1];
+    if (st || n < launched || !(t < base.t_end)) break;
+    // next chunk: the steps the last chunk's average dt predicts, +1
+    const double rate = (t - t_prev) / (double)(n - n_prev);
+    int want = rate > 0.0 ? (int)std::min(4096.0, (base.t_end - t) / rate) + 2 : chunk;
+    chunk = std::max(1, std::min(want, 4 * chunk));
+    t_prev = t;
+    n_prev = n;
+  }
+  // kernels past the end exited without writing: the state is in buffer cur0 ^ (n nsweep)
+  d->cur = cur0 ^ ((n * nsweep) & 1);
+  if (t_out) *t_out = t;
+  if (n_out) *n_out = n;
+  return st;
+}
+
+extern "C" rpl_status rpl_advance_to(rpl_domain* d, double t_end, double cfl, int32_t n_reduced,
+                                     double reduce, int32_t max_steps, double* t_out,
+                                     int32_t* nsteps_out) {
+  if (!d) return fail(RPL_E_INVALID_ARG, "null domain");
+  if (!(cfl > 0.0) || !(t_end >= 0.0) || max_steps < 0)
+    return fail(RPL_E_INVALID_ARG, "cfl > 0, t_end >= 0, max_steps >= 0 required");
+  if (d->g.D == 2 && use_fused(d) && d->cfg.order == 1 && !step2d_has_cfl(d->variant))
+    return fail(RPL_E_INVALID_ARG, "RPL_VARIANT %d has no device-side CFL step", d->variant);
+  CU(cudaSetDevice(d->device));
+  if (d->ghosts_stale) {
+    rpl_status st = rpl_fill_padding(d);
+    if (st) return st;
+  }
+  CflArgs cf;
+  memset(&cf, 0, sizeof(cf));
+  cf.dev = d->d_cfl;
+  cf.t_end = t_end;
+  cf.cfl = cfl;
+  cf.reduce = reduce;
+  cf.n_reduced = n_reduced;
+  cf.gamma = d->cfg.gamma;
+  double dxmin = d->cfg.dx[0];
+  for (int k = 1; k < d->g.D; ++k)
+    if (d->cfg.dx[k] < dxmin) dxmin = d->cfg.dx[k];
+  cf.dxmin = dxmin;
+  for (int k = 0; k < 3; ++k) cf.dx[k] = k < d->g.D ? d->cfg.dx[k] : 0.0;
+  if (t_out) *t_out = 0.0;
+  if (nsteps_out) *nsteps_out = 0;
+  if (max_steps == 0 || !(t_end > 0.0)) return RPL_OK;
+  return d->g.elem == 8 ? advance_to_t<double>(d, cf, max_steps, t_out, nsteps_out)
+                        : advance_to_t<float>(d, cf, max_steps, t_out, nsteps_out);
 }
 
 extern "C" rpl_status rpl_synchronize(rpl_domain* d) {

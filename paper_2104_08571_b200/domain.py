@@ -30,7 +30,7 @@ def _bc(v):
 
 def make_config(size, pad=2, parts=None, dtype="f64", layout="soa", kernel="fused", gamma=1.4,
                 dx=None, bc_lo=None, bc_hi=None, nranks=1, rank=0, nccl_id=None, device=0,
-                stream=None, arena=None, rows_per_chunk=0, transport="nccl"):
+                stream=None, arena=None, rows_per_chunk=0, transport="nccl", order=1):
     size = [int(v) for v in size]
     D = len(size)
     if not 1 <= D <= 3:
@@ -58,6 +58,7 @@ def make_config(size, pad=2, parts=None, dtype="f64", layout="soa", kernel="fuse
     cfg.arena = int(arena) if arena else None
     cfg.rows_per_chunk = int(rows_per_chunk)
     cfg.transport = {"nccl": N.TRANSPORT_NCCL, "p2p": N.TRANSPORT_P2P}[transport]
+    cfg.order = int(order)
     return cfg
 
 
@@ -183,6 +184,15 @@ class Domain:
         N.check(N.lib().rpl_advance_cfl(self._h, float(t_end), float(cfl), int(n_reduced),
                                         float(reduce), int(max_steps), ctypes.byref(n)))
         return n.value
+
+    def advance_to(self, t_end, cfl=0.9, n_reduced=5, reduce=0.2, max_steps=10_000_000):
+        """Device-side CFL run (rpl_advance_to).  Returns (t reached, steps taken)."""
+        t = ctypes.c_double(0.0)
+        n = ctypes.c_int32(0)
+        N.check(N.lib().rpl_advance_to(self._h, float(t_end), float(cfl), int(n_reduced),
+                                       float(reduce), int(max_steps), ctypes.byref(t),
+                                       ctypes.byref(n)))
+        return t.value, n.value
 
     def synchronize(self):
         N.check(N.lib().rpl_synchronize(self._h))

@@ -133,3 +133,14 @@ def test_halo_plan_edge_counts_slabs():
     assert len(xch) == 6
     plan1 = R.halo_plan(size=(16,), pad=2, parts=(1,))
     assert all(e["src_part"] == e["dst_part"] for e in plan1)
+
+
+def test_order2_config_checks():
+    """order 2 needs pad >= 2 (stencil radius 2); order must be 1 or 2 (host only)."""
+    from paper_2104_08571_b200 import _native as N
+    R.config_check(size=(64, 32), pad=2, order=2)
+    with pytest.raises(N.RplError) as e:
+        R.config_check(size=(64, 32), pad=1, order=2)
+    assert "RPL_E_PAD_TOO_SMALL" in str(e.value)
+    with pytest.raises(N.RplError):
+        R.config_check(size=(64, 32), pad=2, order=3)

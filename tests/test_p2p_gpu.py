@@ -21,7 +21,7 @@ def _port():
     return p
 
 
-def _rank(rank, world, port, n, parts, kw, steps, q):
+def _rank(rank, world, port, n, parts, kw, steps, q, t_end=None):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch
@@ -45,8 +45,11 @@ def _rank(rank, world, port, n, parts, kw, steps, q):
         if kw.get("dtype") == "f32":
             U = U.astype(np.float32)
         dom.set_state(U)
-        s = dom.max_wavespeed()
-        dom.advance(0.4 * dx[0] / s, steps)
+        if t_end is None:
+            s = dom.max_wavespeed()
+            dom.advance(0.4 * dx[0] / s, steps)
+        else:
+            s = dom.advance_to(t_end)   # (t reached, steps taken)
         out = dom.get_state()
         q.put((rank, dom.lo, dom.hi, out, s))
         dom.close()
@@ -55,7 +58,7 @@ def _rank(rank, world, port, n, parts, kw, steps, q):
         dist.destroy_process_group()
 
 
-def _single(n, kw, steps):
+def _single(n, kw, steps, t_end=None):
     import paper_2104_08571_b200 as R
     import workloads as W
     D = len(n)
@@ -65,8 +68,11 @@ def _single(n, kw, steps):
         U = U.astype(np.float32)
     with R.Domain(n, dx=dx, **kw) as dom:
         dom.set_state(U)
-        s = dom.max_wavespeed()
-        dom.advance(0.4 * dx[0] / s, steps)
+        if t_end is None:
+            s = dom.max_wavespeed()
+            dom.advance(0.4 * dx[0] / s, steps)
+        else:
+            s = dom.advance_to(t_end)
         return dom.get_state(), s
 
 
@@ -77,19 +83,33 @@ def _single(n, kw, steps):
     ((40, 32, 24), (2, 2, 1), {}),
 ])
 def test_p2p_ranks_bitwise_equal_single_rank(n, parts, kw):
+    _check(n, parts, kw, None)
+
+
+@pytest.mark.parametrize("n,parts,kw", [
+    ((130, 64), (1, 2), {}),
+    ((130, 64), (2, 2), dict(kernel="split")),
+    ((40, 32, 24), (1, 1, 2), {}),
+])
+def test_p2p_device_cfl_bitwise_equal_single_rank(n, parts, kw):
+    """rpl_advance_to over ranks: the wavespeed slot rides the P2P step sync."""
+    _check(n, parts, kw, 0.02)
+
+
+def _check(n, parts, kw, t_end):
     world = int(np.prod(parts))
     steps = 6
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank, args=(r, world, port, n, parts, kw, steps, q))
+    procs = [ctx.Process(target=_rank, args=(r, world, port, n, parts, kw, steps, q, t_end))
              for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
     for p in procs:
         p.join(timeout=120)
-    ref, s_ref = _single(n, kw, steps)
+    ref, s_ref = _single(n, kw, steps, t_end)
     D = len(n)
     for rank, lo, hi, out, s in res:
         assert s == s_ref
