@@ -225,10 +225,13 @@ rpl_status rpl_halo_plan(const rpl_config* cfg, rpl_halo_edge* edges, int32_t ma
 /* Flux difference of the paper's single-GPU FV benchmark (sec. 7.3,
  * P:1264-1284, Table 4): for every interior cell of the current
  * state, R = sum_d (F_{i+1/2} - F_{i-1/2}) along each dim d, F = FORCE flux at
- * step dt, both faces of every direction evaluated per cell ("all four faces of
- * each cell").  Fills stale ghosts first; writes R into the scratch
- * buffer (the state is unchanged; the next rpl_advance overwrites R).  Not a
- * time integrator.  Enqueued, no host sync. */
+ * step dt.  kernel SPLIT (and 1-D/3-D/AoS): the paper's form, both faces of
+ * every direction evaluated per cell ("all four faces of each cell");
+ * kernel FUSED, 2-D SoA: a TMA-tiled kernel that evaluates every face once and
+ * shares it between its two cells -- bitwise the same R.  Fills stale ghosts
+ * first; writes R into the scratch buffer (the state is unchanged; the next
+ * rpl_advance overwrites R).  Not a time integrator.  Enqueued, no
+ * host sync. */
 rpl_status rpl_flux_difference(rpl_domain* dom, double dt);
 
 /* Copy R of the last rpl_flux_difference to host (dense SoA, like rpl_get_state). */

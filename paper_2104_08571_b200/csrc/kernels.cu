@@ -623,10 +623,14 @@ __global__ void __launch_bounds__(32 * NW, MB)
     issue(1);
   }
   int bad = 0, nan = 0;
+  // tile t = blockIdx.x + i G  <->  (win, yb) = (t % nwin, t / nwin), advanced
+  // incrementally (no per-tile integer division)
+  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
+  int win = (int)blockIdx.x % nwin, yb = (int)blockIdx.x / nwin;
+  const int nyb = ntiles / nwin;
+  const int64_t cs = g.cstride;
   for (int i = 0;; ++i) {
-    const int tile = blockIdx.x + i * G;
-    if (tile >= ntiles) break;
-    const int win = tile % nwin, yb = tile / nwin;
+    if (yb >= nyb) break;
     const int xw = win * (W - 2) - 1;
     const int yr = yb * (NW - 2) - 1 + warp;
     const bool row_in = yr <= SY;
@@ -742,7 +746,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
     __syncthreads();  // (B) y-faces published
     // ---- update + store
     if (row_out) {
-      T* dst = a.out + g.row(yr, 0) * g.rstride + g.xo + xw + V * lane;
+      T* dst = a.out + ((int64_t)((int)g.off[1] + yr) * g.rstride + (int)g.xo + xw + V * lane);
       const T* fu = fy + warp * C * W + V * lane;
       T o[V][C];
 #pragma unroll
@@ -768,19 +772,24 @@ __global__ void __launch_bounds__(32 * NW, MB)
             VT w;
             w.x = o[0][c];
             w.y = o[1][c];
-            *reinterpret_cast<VT*>(dst + c * g.cstride) = w;
+            *reinterpret_cast<VT*>(dst + c * cs) = w;
           }
         } else {
 #pragma unroll
           for (int v = 0; v < V; ++v)
             if (ok[v])
 #pragma unroll
-              for (int c = 0; c < C; ++c) dst[c * g.cstride + v] = o[v][c];
+              for (int c = 0; c < C; ++c) dst[c * cs + v] = o[v][c];
         }
       } else {
-        if (ok[0])
+        if (ok[0]) {
+          T* p = dst;
 #pragma unroll
-          for (int c = 0; c < C; ++c) dst[c * g.cstride] = o[0][c];
+          for (int c = 0; c < C; ++c) {
+            *p = o[0][c];
+            p += cs;
+          }
+        }
       }
       const bool yface = (yr < g.pad) | (yr >= SY - g.pad);
 #pragma unroll
@@ -792,6 +801,12 @@ __global__ void __launch_bounds__(32 * NW, MB)
           if (yface | (xv < g.pad) | (xv >= SX - g.pad)) images<D, 0>(a, xv, yr, 0, o[v]);
         }
       }
+    }
+    win += Gr;
+    yb += Gq;
+    if (win >= nwin) {
+      win -= nwin;
+      ++yb;
     }
   }
   if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
@@ -1992,6 +2007,165 @@ __global__ void __launch_bounds__(256) k_fluxdiff(const __grid_constant__ KArgs<
     store_cell<D, L>(g, a.out, x, y, z, R);
   }
 }
+
+// ---------------------------------------------------------------------------
+// f2, tiled 2-D SoA form: every face computed once.  Persistent CTAs of NW
+// warps stream [NW rows][C][32+AL] boxes (TMA, 2-stage ring); warp j owns row
+// y0 - 1 + j.  Per row: F_x, F_y of every cell; x-face l+1/2 via shuffles (the
+// lane's right face, left face from the neighbour lane); (U, F_y) published,
+// y-face between rows j-1 and j computed once and published; rows 1..NW-2 sum
+// R = (dPhi_x) / lam_x + (dPhi_y) / lam_y with exactly k_fluxdiff's operations,
+// so both kernels agree bitwise.  One read of U, one write of R per cell.
+// ---------------------------------------------------------------------------
+template <typename T, int NW>
+struct SmemFD {
+  static constexpr int W = 32, C = 4;
+  static constexpr int AL = 16 / (int)sizeof(T);
+  static constexpr int WB = W + AL;
+  static constexpr int STAGE = NW * C * WB;
+  static constexpr int UF = NW * 2 * C * W;
+  static constexpr int FY = NW * C * W;
+  static constexpr size_t bytes() { return (size_t)(2 * STAGE + UF + FY) * sizeof(T) + 64; }
+};
+
+template <typename T, int NW, int MB>
+__global__ void __launch_bounds__(32 * NW, MB)
+    k_fluxdiff_pt(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
+                  int nwin, int ntiles) {
+  constexpr int D = 2, C = 4, W = 32;
+  using SM = SmemFD<T, NW>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  T* stage = reinterpret_cast<T*>(smem);
+  T* uf = stage + 2 * SM::STAGE;
+  T* fyb = uf + SM::UF;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + SM::FY);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int SX = (int)g.S[0], SY = (int)g.S[1];
+  const int G = gridDim.x;
+  const T gm1 = a.gm1;
+  const T ilx = T(0.25) / a.q[0], ily = T(0.25) / a.q[1];
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int i) {
+    const int tile = blockIdx.x + i * G;
+    if (tile >= ntiles) return;
+    const int s = i & 1;
+    const int w = tile % nwin, yb = tile / nwin;
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
+    const int x0 = (int)g.xo + w * (W - 2) - 1;
+    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
+                 (int)g.off[1] + yb * (NW - 2) - 1, 0);
+  };
+  if (threadIdx.x == 0) {
+    issue(0);
+    issue(1);
+  }
+  for (int i = 0;; ++i) {
+    const int tile = blockIdx.x + i * G;
+    if (tile >= ntiles) break;
+    const int win = tile % nwin, yb = tile / nwin;
+    const int xw = win * (W - 2) - 1;
+    const int yr = yb * (NW - 2) - 1 + warp;
+    const int s = i & 1;
+    mbar_wait(&bar[s], (i >> 1) & 1);
+    T U[C], Fx[C], Fy[C], Rx[C];
+    {
+      const int sh = ((int)g.xo + xw) % SM::AL;
+      const T* st = stage + s * SM::STAGE + warp * C * SM::WB + sh + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) U[c] = st[c * SM::WB];
+    }
+    phys_flux<D, 0>(U, Fx, gm1);
+    phys_flux<D, 1>(U, Fy, gm1);
+    {
+      T Un[C], Fn[C], Pnx[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Un[c] = __shfl_down_sync(kFull, U[c], 1);
+        Fn[c] = __shfl_down_sync(kFull, Fx[c], 1);
+      }
+      force_face<D, 0>(U, Fx, Un, Fn, Pnx, a.q[0], a.nq2[0], gm1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const T Ppv = __shfl_up_sync(kFull, Pnx[c], 1);
+        Rx[c] = fma(Pnx[c] - Ppv, ilx, T(0));
+      }
+    }
+    {
+      T* w = uf + warp * 2 * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        w[c * W] = U[c];
+        w[(C + c) * W] = Fy[c];
+      }
+    }
+    __syncthreads();  // (A) stage consumed, (U, F_y) published
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      issue(i + 2);
+    }
+    T Py[C];
+    if (warp >= 1) {
+      T Up[C], Fp[C];
+      const T* r = uf + (warp - 1) * 2 * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Up[c] = r[c * W];
+        Fp[c] = r[(C + c) * W];
+      }
+      force_face<D, 1>(Up, Fp, U, Fy, Py, a.q[1], a.nq2[1], gm1);
+      T* fw = fyb + warp * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) fw[c * W] = Py[c];
+    }
+    __syncthreads();  // (B) y-faces published
+    if (warp >= 1 && warp <= NW - 2 && yr < SY && lane >= 1 && lane <= 30 && xw + lane < SX) {
+      const T* fu = fyb + (warp + 1) * C * W + lane;
+      T* dst = a.out + g.row(yr, 0) * g.rstride + g.xo + xw + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) dst[c * g.cstride] = fma(fu[c * W] - Py[c], ily, Rx[c]);
+    }
+  }
+}
+
+template <typename T, int NW, int MB>
+static void launch_fd_pt(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  constexpr int W = 32;
+  using SM = SmemFD<T, NW>;
+  const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
+  const int nyb = (int)((a.g.S[1] + (NW - 2) - 1) / (NW - 2));
+  const int ntiles = nwin * nyb;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(k_fluxdiff_pt<T, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SM::bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fluxdiff_pt<T, NW, MB>, 32 * NW,
+                                                  SM::bytes());
+    if (per_sm < 1) per_sm = 1;
+  }
+  int nsm = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int grid = per_sm * nsm;
+  if (grid > ntiles) grid = ntiles;
+  k_fluxdiff_pt<T, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
+}
+
+int fd_tile_rows(int elem) { return 16; }
+
+template <typename T>
+void launch_fluxdiff_tiled(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  if (sizeof(T) == 4) return launch_fd_pt<T, 16, 2>(a, tmap, s);
+  return launch_fd_pt<T, 16, 2>(a, tmap, s);
+}
+template void launch_fluxdiff_tiled<float>(const KArgs<float>&, const void*, cudaStream_t);
+template void launch_fluxdiff_tiled<double>(const KArgs<double>&, const void*, cudaStream_t);
 
 template <typename T>
 void launch_fluxdiff(const KArgs<T>& a, cudaStream_t s) {

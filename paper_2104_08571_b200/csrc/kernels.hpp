@@ -29,6 +29,9 @@ void launch_maxws(const Geom& g, const T* in, double gamma, unsigned long long* 
 
 template <typename T>
 void launch_fluxdiff(const KArgs<T>& a, cudaStream_t s);  // sec. 7.3 flux difference (f2)
+template <typename T>  // tiled 2-D SoA form (TMA box {32+AL, C, fd_tile_rows, 1})
+void launch_fluxdiff_tiled(const KArgs<T>& a, const void* tmap, cudaStream_t s);
+int fd_tile_rows(int elem);
 
 // 2-D variants whose kernel implements the device-side CFL step (k_step2d_pt)
 inline bool step2d_has_cfl(int variant) { return variant == 0 || (variant >= 30 && variant <= 39) || variant == 44 || variant == 46 ||

@@ -231,6 +231,8 @@ struct rpl_domain {
   };
   TMap tmap[2][kMaxParts];
   bool tmaps_ok = false;
+  TMap tmap_fd[2][kMaxParts];  // tiled flux-difference kernel (lazy)
+  bool fd_tmaps = false;
   // P2P transport
   unsigned long long* ctl = nullptr;        // [0,64): step flags from each rank, then 4 sets of
                                             // [64] wavespeed slots (set 0: rpl_max_wavespeed,
@@ -1116,13 +1118,24 @@ static rpl_status fluxdiff_t(rpl_domain* d, double dt) {
   }
   a.gm1 = (T)(d->cfg.gamma - 1.0);
   a.flag = d->d_flag;
+  // fused config, 2-D SoA: tiled kernel (each face once); otherwise the plain one
+  const bool tiled = d->cfg.kernel == RPL_KERNEL_FUSED && g.D == 2 && g.layout == 0;
+  if (tiled && !d->fd_tmaps) {
+    for (int p : d->local)
+      for (int b = 0; b < 2; ++b)
+        if (make_tmap(g, d->buf[b][p], d->tmap_fd[b][p].b, 32 + 16 / g.elem,
+                      fd_tile_rows(g.elem)) != 0)
+          return fail(RPL_E_CUDA, "cuTensorMapEncodeTiled failed for the flux-difference kernel");
+    d->fd_tmaps = true;
+  }
   for (int p : d->local) {
     a.part = p;
     g.part_coords(p, a.pc);
     for (int k = 0; k < 3; ++k) a.lo[k] = a.pc[k] * g.S[k];
     a.in = (const T*)d->buf[d->cur][p];
     a.out = (T*)d->buf[d->cur ^ 1][p];
-    launch_fluxdiff<T>(a, d->stream);
+    if (tiled) launch_fluxdiff_tiled<T>(a, d->tmap_fd[d->cur][p].b, d->stream);
+    else launch_fluxdiff<T>(a, d->stream);
   }
   CU(cudaGetLastError());
   return RPL_OK;

@@ -316,3 +316,22 @@ def test_flux_difference_matches_oracle(dtype, tol, n):
     # R is a difference of O(1) fluxes: measure against the flux scale, not R itself
     scale = np.max(np.abs(U0.astype(np.float64))) / min(dx) * 10
     assert np.max(np.abs(Rg.astype(np.float64) - Ro.astype(np.float64))) <= tol * scale
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("n,pad,parts", [((130, 70), 2, (1, 1)), ((1000, 333), 1, (1, 1)),
+                                         ((256, 96), 1, (2, 2))])
+def test_flux_difference_tiled_equals_plain_bitwise(dtype, n, pad, parts):
+    """f2: the tiled 2-D kernel (each face once) and the paper's per-cell form
+    (kernel=split) give bitwise the same R (same operations per face and sum)."""
+    dx = [1.0 / n[0]] * 2
+    U0 = W.shock_bubble(n, dx=dx)
+    if dtype == "f32":
+        U0 = U0.astype(np.float32)
+    out = []
+    for kernel in ("fused", "split"):
+        with R.Domain(n, pad=pad, parts=parts, dtype=dtype, dx=dx, kernel=kernel) as dom:
+            dom.set_state(U0)
+            dom.flux_difference(2e-4)
+            out.append(dom.get_flux_difference())
+    assert np.array_equal(out[0], out[1])
