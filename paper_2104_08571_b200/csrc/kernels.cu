@@ -909,10 +909,11 @@ __global__ void __launch_bounds__(32 * NW, MB)
   int bad = 0, nan = 0;
   const bool lane_in = (lane >= 1) & (lane <= 30);   // has both x-neighbours
   const bool lane_out = (lane >= 2) & (lane <= 29);  // U* valid
+  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
+  int win = (int)blockIdx.x % nwin, yb = (int)blockIdx.x / nwin;
+  const int nyb = ntiles / nwin;
   for (int i = 0;; ++i) {
-    const int tile = blockIdx.x + i * G;
-    if (tile >= ntiles) break;
-    const int win = tile % nwin, yb = tile / nwin;
+    if (yb >= nyb) break;
     const int xw = win * (W - 4) - 2;
     const int yr = yb * (NW - 4) - 2 + warp;
     const int xv = xw + lane;
@@ -1000,13 +1001,23 @@ __global__ void __launch_bounds__(32 * NW, MB)
       T o[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) o[c] = S_[c] - (fu[c * W] - Py[c]);
-      T* dst = a.out + g.row(yr, 0) * g.rstride + g.xo + xv;
+      T* dst = a.out + ((int64_t)((int)g.off[1] + yr) * g.rstride + (int)g.xo + xv);
+      const int64_t cs = g.cstride;
 #pragma unroll
-      for (int c = 0; c < C; ++c) dst[c * g.cstride] = o[c];
+      for (int c = 0; c < C; ++c) {
+        *dst = o[c];
+        dst += cs;
+      }
       nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
       if (ws) wmax = fmax(wmax, wavespeed<D>(o, gm1, gam));
       if ((yr < g.pad) | (yr >= SY - g.pad) | (xv < g.pad) | (xv >= SX - g.pad))
         images<D, 0>(a, xv, yr, 0, o);
+    }
+    win += Gr;
+    yb += Gq;
+    if (win >= nwin) {
+      win -= nwin;
+      ++yb;
     }
   }
   if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
@@ -1697,9 +1708,9 @@ int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
   switch (variant) {
     case 30: *box_w = 32 + al; *box_rows = 16; return 1;
     case 31: *box_w = 64 + al; *box_rows = 8; return 1;
-    case 0: case 32: case 34: case 35: *box_w = 32 + al; *box_rows = 8; return 1;
+    case 32: case 34: case 35: *box_w = 32 + al; *box_rows = 8; return 1;
     case 36: *box_w = 64 + al; *box_rows = 8; return 1;
-    case 37: case 39: *box_w = 32 + al; *box_rows = 12; return 1;
+    case 0: case 37: case 39: *box_w = 32 + al; *box_rows = 12; return 1;
     case 38: *box_w = 32 + al; *box_rows = 10; return 1;
     case 44: *box_w = 32 + al; *box_rows = 24; return 1;
     case 46: *box_w = 32 + al; *box_rows = 14; return 1;
@@ -1873,7 +1884,7 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 31: return launch_pt2d<T, 2, 8>(a, tmap, s);
     case 32: return launch_pt2d<T, 1, 8>(a, tmap, s);
     case 33: return launch_pt2d<T, 2, 16>(a, tmap, s);
-    case 0: case 34: return launch_pt2d<T, 1, 8, 3>(a, tmap, s);
+    case 34: return launch_pt2d<T, 1, 8, 3>(a, tmap, s);
     case 40: return launch_cm2d<T, 1, 8, 3>(a, tmap, s);
     case 60: return launch_pp2d<T, 1, 8, 3>(a, tmap, s);
     case 61: return launch_pp2d<T, 1, 8, 2>(a, tmap, s);
@@ -1884,7 +1895,7 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 43: return launch_cm2d<T, 1, 16, 1>(a, tmap, s);
     case 35: return launch_pt2d<T, 1, 8, 4>(a, tmap, s);
     case 36: return launch_pt2d<T, 2, 8, 2>(a, tmap, s);
-    case 37: return launch_pt2d<T, 1, 12, 2>(a, tmap, s);
+    case 0: case 37: return launch_pt2d<T, 1, 12, 2>(a, tmap, s);  // default (DESIGN.md tuning)
     case 38: return launch_pt2d<T, 1, 10, 3>(a, tmap, s);
     case 39: return launch_pt2d<T, 1, 12, 3>(a, tmap, s);
     case 44: return launch_pt2d<T, 1, 24, 1>(a, tmap, s);
@@ -2065,10 +2076,11 @@ __global__ void __launch_bounds__(32 * NW, MB)
     issue(0);
     issue(1);
   }
+  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
+  int win = (int)blockIdx.x % nwin, yb = (int)blockIdx.x / nwin;
+  const int nyb = ntiles / nwin;
   for (int i = 0;; ++i) {
-    const int tile = blockIdx.x + i * G;
-    if (tile >= ntiles) break;
-    const int win = tile % nwin, yb = tile / nwin;
+    if (yb >= nyb) break;
     const int xw = win * (W - 2) - 1;
     const int yr = yb * (NW - 2) - 1 + warp;
     const int s = i & 1;
@@ -2126,9 +2138,19 @@ __global__ void __launch_bounds__(32 * NW, MB)
     __syncthreads();  // (B) y-faces published
     if (warp >= 1 && warp <= NW - 2 && yr < SY && lane >= 1 && lane <= 30 && xw + lane < SX) {
       const T* fu = fyb + (warp + 1) * C * W + lane;
-      T* dst = a.out + g.row(yr, 0) * g.rstride + g.xo + xw + lane;
+      T* dst = a.out + ((int64_t)((int)g.off[1] + yr) * g.rstride + (int)g.xo + xw + lane);
+      const int64_t cs = g.cstride;
 #pragma unroll
-      for (int c = 0; c < C; ++c) dst[c * g.cstride] = fma(fu[c * W] - Py[c], ily, Rx[c]);
+      for (int c = 0; c < C; ++c) {
+        *dst = fma(fu[c * W] - Py[c], ily, Rx[c]);
+        dst += cs;
+      }
+    }
+    win += Gr;
+    yb += Gq;
+    if (win >= nwin) {
+      win -= nwin;
+      ++yb;
     }
   }
 }
