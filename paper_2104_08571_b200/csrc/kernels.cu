@@ -813,6 +813,351 @@ __global__ void __launch_bounds__(32 * NW, MB)
   if (ws) publish_max(a, wmax);
 }
 
+// ---------------------------------------------------------------------------
+// K-B (2-D), low-register form of k_step2d_pt (V = 1): no value stays in
+// registers across a CTA barrier -- the Y phase re-reads the row's own (U*, F_y)
+// and the update re-reads U* and both y-faces from shared memory -- so each
+// phase's live set is its own, for 64-register builds (32 warps / SM).  Same
+// arithmetic as k_step2d_pt, bitwise identical results.
+// ---------------------------------------------------------------------------
+template <typename T, int NW, int MB>
+__global__ void __launch_bounds__(32 * NW, MB)
+    k_step2d_lr(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
+                int nwin, int ntiles) {
+  constexpr int D = 2, C = 4, W = 32;
+  using SM = SmemPT<T, 1, NW>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  T* stage = reinterpret_cast<T*>(smem);
+  T* xy = stage + 2 * SM::STAGE;
+  T* fy = xy + SM::XY;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fy + SM::FY);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int SX = (int)g.S[0], SY = (int)g.S[1];
+  const int G = gridDim.x;
+  Coef<T> kc;
+  if (!step_coef(a, kc)) return;
+  const bool ws = a.cf.dev != nullptr;
+  const T gam = (T)a.cf.gamma;
+  T wmax = T(0);
+  const T gm1 = a.gm1;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int i) {
+    const int tile = blockIdx.x + i * G;
+    if (tile >= ntiles) return;
+    const int s = i & 1;
+    const int w = tile % nwin, yb = tile / nwin;
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
+    const int x0 = (int)g.xo + w * (W - 2) - 1;
+    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
+                 (int)g.off[1] + yb * (NW - 2) - 1, 0);
+  };
+  if (threadIdx.x == 0) {
+    issue(0);
+    issue(1);
+  }
+  int bad = 0, nan = 0;
+  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
+  int win = (int)blockIdx.x % nwin, yb = (int)blockIdx.x / nwin;
+  const int nyb = ntiles / nwin;
+  const int64_t cs = g.cstride;
+  T* const xr = xy + warp * 2 * C * W + lane;  // this row's (U*, F_y)
+  for (int i = 0;; ++i) {
+    if (yb >= nyb) break;
+    const int xw = win * (W - 2) - 1;
+    const int yr = yb * (NW - 2) - 1 + warp;
+    const int xv = xw + lane;
+    const bool row_in = yr <= SY;
+    const int s = i & 1;
+    mbar_wait(&bar[s], (i >> 1) & 1);
+    // ---- X
+    {
+      T U[C], F[C];
+      const int sh = ((int)g.xo + xw) % SM::AL;
+      const T* st = stage + s * SM::STAGE + warp * C * SM::WB + sh + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) U[c] = st[c * SM::WB];
+      const int b0 = phys_flux<D, 0>(U, F, gm1);
+      bad |= ((xv >= -1) & (xv <= SX) & row_in) ? b0 : 0;
+      T Pnx[C];
+      {
+        T Un[C], Fn[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          Un[c] = __shfl_down_sync(kFull, U[c], 1);
+          Fn[c] = __shfl_down_sync(kFull, F[c], 1);
+        }
+        force_face<D, 0>(U, F, Un, Fn, Pnx, kc.q[0], kc.nq2[0], gm1);
+      }
+      T S_[C], G_[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const T Ppv = __shfl_up_sync(kFull, Pnx[c], 1);
+        S_[c] = U[c] - (Pnx[c] - Ppv);
+      }
+      const int b1 = phys_flux<D, 1>(S_, G_, gm1);
+      bad |= ((lane >= 1) & (lane <= W - 2) & (xv < SX) & row_in) ? b1 : 0;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        xr[c * W] = S_[c];
+        xr[(C + c) * W] = G_[c];
+      }
+    }
+    __syncthreads();  // (A) stage s consumed; (U*, F_y) published
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      issue(i + 2);
+    }
+    // ---- Y face between rows warp-1 and warp
+    if (warp >= 1) {
+      T Sp[C], Gp[C], S_[C], G_[C], Py[C];
+      const T* pr = xr - 2 * C * W;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Sp[c] = pr[c * W];
+        Gp[c] = pr[(C + c) * W];
+        S_[c] = xr[c * W];
+        G_[c] = xr[(C + c) * W];
+      }
+      force_face<D, 1>(Sp, Gp, S_, G_, Py, kc.q[1], kc.nq2[1], gm1);
+      T* fw = fy + (warp - 1) * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) fw[c * W] = Py[c];
+    }
+    __syncthreads();  // (B) y-faces published
+    // ---- update + store
+    if ((warp >= 1) & (warp <= NW - 2) & (yr < SY) & (lane >= 1) & (lane <= W - 2) & (xv < SX)) {
+      const T* fd = fy + (warp - 1) * C * W + lane;  // face below (j - 1/2)
+      T o[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) o[c] = xr[c * W] - (fd[(c + C) * W] - fd[c * W]);
+      T* dst = a.out + ((int64_t)((int)g.off[1] + yr) * g.rstride + (int)g.xo + xv);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        *dst = o[c];
+        dst += cs;
+      }
+      nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
+      if (ws) wmax = fmax(wmax, wavespeed<D>(o, gm1, gam));
+      if ((yr < g.pad) | (yr >= SY - g.pad) | (xv < g.pad) | (xv >= SX - g.pad))
+        images<D, 0>(a, xv, yr, 0, o);
+    }
+    win += Gr;
+    yb += Gq;
+    if (win >= nwin) {
+      win -= nwin;
+      ++yb;
+    }
+  }
+  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
+}
+
+template <typename T, int NW, int MB>
+static void launch_lr2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  constexpr int W = 32;
+  using SM = SmemPT<T, 1, NW>;
+  const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
+  const int nyb = (int)((a.g.S[1] + (NW - 2) - 1) / (NW - 2));
+  const int ntiles = nwin * nyb;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(k_step2d_lr<T, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SM::bytes());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step2d_lr<T, NW, MB>, 32 * NW,
+                                                  SM::bytes());
+    if (per_sm < 1) per_sm = 1;
+  }
+  int nsm = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int grid = per_sm * nsm;
+  if (grid > ntiles) grid = ntiles;
+  k_step2d_lr<T, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
+}
+
+// ---------------------------------------------------------------------------
+// K-B (2-D), warp-march form: no CTA barriers, no shared-memory hand-offs.
+// Each warp independently owns tasks = (32-slot x-window, chunk of R rows) and
+// marches down the chunk's rows y0-1 .. y1 (y1 = min(y0+R, SY)): per row it
+// x-sweeps in registers (shuffles), forms the y-face with the previous row's
+// (U*, F_y) held in registers, and updates + stores the previous row.  Rows
+// arrive through a per-warp DEPTH-slot TMA ring (box = one row, C components),
+// prefetched DEPTH rows ahead across task boundaries.  Same arithmetic as
+// k_step2d_pt (bitwise identical results).
+// ---------------------------------------------------------------------------
+template <typename T>
+struct WMRow {
+  static constexpr int W = 32, C = 4, AL = 16 / (int)sizeof(T), WB = W + AL;
+  static constexpr int ELEMS = C * WB;  // one TMA row box
+  // slot stride: TMA tensor destinations must be 128-byte aligned
+  static constexpr int SLOT = ((ELEMS * (int)sizeof(T) + 127) / 128) * 128 / (int)sizeof(T);
+};
+
+template <typename T, int DEPTH, int NWB, int MB>
+__global__ void __launch_bounds__(32 * NWB, MB)
+    k_step2d_wm(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
+                int nwin, int R, int ntask) {
+  constexpr int D = 2, C = 4, W = 32;
+  using RW = WMRow<T>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* ring = reinterpret_cast<T*>(smem) + warp * DEPTH * RW::SLOT;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<T*>(smem) + NWB * DEPTH * RW::SLOT) +
+                  warp * DEPTH;
+  const Geom& g = a.g;
+  const int SX = (int)g.S[0], SY = (int)g.S[1];
+  Coef<T> kc;
+  if (!step_coef(a, kc)) return;
+  const bool ws = a.cf.dev != nullptr;
+  const T gam = (T)a.cf.gamma;
+  T wmax = T(0);
+  const T gm1 = a.gm1;
+  const int gw = blockIdx.x * NWB + warp, nw = gridDim.x * NWB;
+  if (gw >= ntask) return;  // warp-uniform; no CTA-wide synchronisation below
+  if (lane == 0) {
+    for (int j = 0; j < DEPTH; ++j) mbar_init(&bar[j], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  // producer cursor (lane 0): task pt, row index pr within it
+  int pt = gw, pr = 0;
+  auto task_rows = [&](int t) {
+    const int y0 = (t / nwin) * R;
+    return min(y0 + R, SY) - y0 + 2;  // rows y0-1 .. y1
+  };
+  auto produce = [&](int slot) {  // lane 0: next row of the stream into slot
+    if (pt >= ntask) return;
+    const int win = pt % nwin, y0 = (pt / nwin) * R;
+    const int x0 = (int)g.xo + win * (W - 2) - 1;
+    mbar_arrive_expect_tx(&bar[slot], RW::ELEMS * (unsigned)sizeof(T));
+    tma_load_box(ring + slot * RW::SLOT, &tmap, &bar[slot], x0 - x0 % RW::AL, 0,
+                 (int)g.off[1] + y0 - 1 + pr, 0);
+    if (++pr == task_rows(pt)) {
+      pr = 0;
+      pt += nw;
+    }
+  };
+  if (lane == 0)
+    for (int j = 0; j < DEPTH; ++j) produce(j);
+  int bad = 0, nan = 0;
+  const int64_t cs = g.cstride;
+  unsigned k = 0;  // stream position (row counter of this warp)
+  for (int t = gw; t < ntask; t += nw) {
+    const int win = t % nwin, y0 = (t / nwin) * R;
+    const int y1 = min(y0 + R, SY);
+    const int xw = win * (W - 2) - 1;
+    const int xv = xw + lane;
+    const bool x_in = (xv >= -1) & (xv <= SX);
+    const bool x_out = (lane >= 1) & (lane <= W - 2) & (xv < SX);
+    const int sh = ((int)g.xo + xw) % RW::AL;
+    T Sp[C], Gp[C], Pp[C];  // previous row: U*, F_y(U*), face below it
+    for (int yr = y0 - 1; yr <= y1; ++yr, ++k) {
+      const int slot = k % DEPTH;
+      mbar_wait(&bar[slot], (k / DEPTH) & 1);
+      T U[C], F[C], S_[C], G_[C];
+      {
+        const T* st = ring + slot * RW::SLOT + sh + lane;
+#pragma unroll
+        for (int c = 0; c < C; ++c) U[c] = st[c * RW::WB];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        fence_proxy_async();
+        produce(slot);
+      }
+      const int b0 = phys_flux<D, 0>(U, F, gm1);
+      bad |= x_in ? b0 : 0;
+      {
+        T Pnx[C], Un[C], Fn[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          Un[c] = __shfl_down_sync(kFull, U[c], 1);
+          Fn[c] = __shfl_down_sync(kFull, F[c], 1);
+        }
+        force_face<D, 0>(U, F, Un, Fn, Pnx, kc.q[0], kc.nq2[0], gm1);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const T Ppv = __shfl_up_sync(kFull, Pnx[c], 1);
+          S_[c] = U[c] - (Pnx[c] - Ppv);
+        }
+      }
+      const int b1 = phys_flux<D, 1>(S_, G_, gm1);
+      bad |= x_out ? b1 : 0;
+      if (yr >= y0) {
+        T Py[C];  // face between rows yr-1 and yr
+        force_face<D, 1>(Sp, Gp, S_, G_, Py, kc.q[1], kc.nq2[1], gm1);
+        if (yr >= y0 + 1 && x_out) {  // update and store row yr-1
+          const int yo = yr - 1;
+          T o[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) o[c] = Sp[c] - (Py[c] - Pp[c]);
+          T* dst = a.out + ((int64_t)((int)g.off[1] + yo) * g.rstride + (int)g.xo + xv);
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            *dst = o[c];
+            dst += cs;
+          }
+          nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
+          if (ws) wmax = fmax(wmax, wavespeed<D>(o, gm1, gam));
+          if ((yo < g.pad) | (yo >= SY - g.pad) | (xv < g.pad) | (xv >= SX - g.pad))
+            images<D, 0>(a, xv, yo, 0, o);
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) Pp[c] = Py[c];
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Sp[c] = S_[c];
+        Gp[c] = G_[c];
+      }
+    }
+  }
+  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
+}
+
+// rows per task: one round of tasks over all warp slots when the grid allows
+static int wm_rows(const Geom& g, int warp_slots) {
+  const int nwin = (int)((g.S[0] + 29) / 30);
+  int nc = warp_slots / nwin;
+  if (nc < 1) nc = 1;
+  int R = (int)((g.S[1] + nc - 1) / nc);
+  if (R < 4) R = 4;
+  return R;
+}
+
+template <typename T, int DEPTH, int NWB, int MB>
+static void launch_wm2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  using RW = WMRow<T>;
+  const size_t sm = (size_t)NWB * DEPTH * (RW::SLOT * sizeof(T) + 8) + 64;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(k_step2d_wm<T, DEPTH, NWB, MB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step2d_wm<T, DEPTH, NWB, MB>,
+                                                  32 * NWB, sm);
+    if (per_sm < 1) per_sm = 1;
+  }
+  int nsm = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int slots = per_sm * nsm * NWB;
+  const int nwin = (int)((a.g.S[0] + 29) / 30);
+  const int R = a.rows > 0 ? a.rows : wm_rows(a.g, slots);
+  const int ntask = nwin * (int)((a.g.S[1] + R - 1) / R);
+  int grid = (ntask + NWB - 1) / NWB;
+  if (grid > per_sm * nsm) grid = per_sm * nsm;
+  k_step2d_wm<T, DEPTH, NWB, MB><<<grid, 32 * NWB, sm, s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, R, ntask);
+}
+
 template <typename T, int V, int NW, int MB = (V == 1 ? 2 : 1)>
 static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   constexpr int W = 32 * V;
@@ -1713,6 +2058,12 @@ int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
     case 0: case 37: case 39: *box_w = 32 + al; *box_rows = 12; return 1;
     case 38: *box_w = 32 + al; *box_rows = 10; return 1;
     case 44: *box_w = 32 + al; *box_rows = 24; return 1;
+    case 80: case 83: *box_w = 32 + al; *box_rows = 8; return 1;
+    case 90: case 91: case 92: case 93: case 94: case 95:
+      *box_w = 32 + al; *box_rows = 1; return 1;
+    case 81: *box_w = 32 + al; *box_rows = 16; return 1;
+    case 82: *box_w = 32 + al; *box_rows = 12; return 1;
+    case 84: *box_w = 32 + al; *box_rows = 10; return 1;
     case 46: *box_w = 32 + al; *box_rows = 14; return 1;
     case 47: *box_w = 32 + al; *box_rows = 20; return 1;
     case 40: case 41: *box_w = 32 + al; *box_rows = 8; return 1;
@@ -1899,6 +2250,17 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 38: return launch_pt2d<T, 1, 10, 3>(a, tmap, s);
     case 39: return launch_pt2d<T, 1, 12, 3>(a, tmap, s);
     case 44: return launch_pt2d<T, 1, 24, 1>(a, tmap, s);
+    case 90: return launch_wm2d<T, 3, 8, 3>(a, tmap, s);
+    case 91: return launch_wm2d<T, 4, 8, 3>(a, tmap, s);
+    case 92: return launch_wm2d<T, 3, 8, 4>(a, tmap, s);
+    case 93: return launch_wm2d<T, 6, 8, 3>(a, tmap, s);
+    case 94: return launch_wm2d<T, 3, 8, 2>(a, tmap, s);
+    case 95: return launch_wm2d<T, 4, 16, 1>(a, tmap, s);
+    case 80: return launch_lr2d<T, 8, 4>(a, tmap, s);
+    case 81: return launch_lr2d<T, 16, 2>(a, tmap, s);
+    case 82: return launch_lr2d<T, 12, 2>(a, tmap, s);
+    case 83: return launch_lr2d<T, 8, 3>(a, tmap, s);
+    case 84: return launch_lr2d<T, 10, 3>(a, tmap, s);
     case 46: return launch_pt2d<T, 1, 14, 2>(a, tmap, s);
     case 47: return launch_pt2d<T, 1, 20, 1>(a, tmap, s);
     default: break;

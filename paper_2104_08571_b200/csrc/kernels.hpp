@@ -35,7 +35,8 @@ int fd_tile_rows(int elem);
 
 // 2-D variants whose kernel implements the device-side CFL step (k_step2d_pt)
 inline bool step2d_has_cfl(int variant) { return variant == 0 || (variant >= 30 && variant <= 39) || variant == 44 || variant == 46 ||
-         variant == 47; }
+         variant == 47 || (variant >= 80 && variant <= 84) ||
+         (variant >= 90 && variant <= 95); }
 
 int auto_rows_2d(const Geom& g);
 int auto_rows_3d(const Geom& g);

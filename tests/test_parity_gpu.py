@@ -214,18 +214,21 @@ def test_uniform_state_bitwise_full_size():
     assert np.array_equal(Ug, U0)
 
 
-def _patch_oracle(Uin, lo, hi, n, k, dt, dx, bcs):
-    """Oracle on a sub-box [lo,hi) of the full input; valid region shrinks by k per cut side."""
+def _patch_oracle(Uin, lo, hi, n, k, dt, dx, bcs, order=1):
+    """Oracle on a sub-box [lo,hi) of the full input; the valid region shrinks by
+    (stencil radius) x k per cut side (radius 1 for order 1, 2 for order 2)."""
     D = len(n)
     sl = tuple(slice(lo[d], hi[d]) for d in reversed(range(D)))
     sub = np.ascontiguousarray(Uin[sl])
     pn = tuple(hi[d] - lo[d] for d in range(D))
     g = oracle.Grid(pn, pad=2, dx=dx, bc_lo=[OK[bcs] if lo[d] == 0 else oracle.BC_TRANSMISSIVE
                                              for d in range(D)],
-                    bc_hi=[OK[bcs] if hi[d] == n[d] else oracle.BC_TRANSMISSIVE for d in range(D)])
+                    bc_hi=[OK[bcs] if hi[d] == n[d] else oracle.BC_TRANSMISSIVE for d in range(D)],
+                    order=order)
     out = oracle.step(g, sub, dt, k)
-    v0 = [0 if lo[d] == 0 else k for d in range(D)]
-    v1 = [pn[d] if hi[d] == n[d] else pn[d] - k for d in range(D)]
+    m = k * order
+    v0 = [0 if lo[d] == 0 else m for d in range(D)]
+    v1 = [pn[d] if hi[d] == n[d] else pn[d] - m for d in range(D)]
     vsl = tuple(slice(v0[d], v1[d]) for d in reversed(range(D)))
     gsl = tuple(slice(lo[d] + v0[d], lo[d] + v1[d]) for d in reversed(range(D)))
     return out[vsl], gsl
@@ -335,3 +338,86 @@ def test_flux_difference_tiled_equals_plain_bitwise(dtype, n, pad, parts):
             dom.flux_difference(2e-4)
             out.append(dom.get_flux_difference())
     assert np.array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("variant", ["34", "37", "44", "80", "81", "84", "90", "94", "95"])
+@pytest.mark.parametrize("parts", [(1, 1), (2, 3)])
+def test_2d_kernel_variants_bitwise(variant, parts, monkeypatch):
+    """Every 2-D fused kernel variant (RPL_VARIANT, DESIGN.md tuning log) gives
+    bitwise the split kernel's result (ragged windows and tiles, partitions)."""
+    n = (190, 126)
+    dx = [1.0 / 190] * 2
+    U0 = W.shock_bubble(n, dx=dx)
+    dt = 0.4 * dx[0] / 5.8
+    ref = run_gpu(U0, dt, 7, kernel="split", dx=dx, parts=parts)
+    monkeypatch.setenv("RPL_VARIANT", variant)
+    assert np.array_equal(run_gpu(U0, dt, 7, dx=dx, parts=parts), ref)
+
+
+def _sample_boxes(n, size, count, seed):
+    """Patch origins: the corners plus seeded interior positions."""
+    rng = np.random.default_rng(seed)
+    D = len(n)
+    out = [tuple(0 for _ in range(D)), tuple(n[d] - size for d in range(D))]
+    for _ in range(count):
+        out.append(tuple(int(rng.integers(0, n[d] - size + 1)) for d in range(D)))
+    return out
+
+
+@pytest.mark.parametrize("n,dtype,tol", [((512, 512, 512), "f64", 1e-12),
+                                         ((384, 384, 384), "f32", 1e-4)])
+def test_full_size_sampled_parity_3d(n, dtype, tol):
+    """BASELINE configs[2] (512^3 fp64) and configs[3] (384^3 fp32 per GPU) at full size in
+    the bench's launch configuration: 2 fused steps, sampled 20^3 patches vs the oracle."""
+    dx = [1.0 / n[0]] * 3
+    U0 = W.shock_bubble(n, dx=dx)
+    if dtype == "f32":
+        U0 = U0.astype(np.float32)
+    dt = 0.4 * dx[0] / 5.8
+    k = 2
+    Ug = run_gpu(U0, dt, k, dtype=dtype, dx=dx)
+    for lo in _sample_boxes(n, 20, 4, seed=7) + [(40, n[1] // 2 - 10, n[2] // 2 - 10)]:
+        hi = tuple(lo[d] + 20 for d in range(3))
+        ref, gsl = _patch_oracle(U0, lo, hi, n, k, dt, dx, "clamp")
+        assert relerr(Ug[gsl], ref) <= tol, lo
+
+
+def test_full_size_sampled_parity_order2_2d1024():
+    """f3 at configs[1] size: order-2 fused kernel, sampled patches vs the order-2 oracle."""
+    n = (1024, 1024)
+    dx = [1.0 / 1024] * 2
+    U0 = W.shock_bubble(n, dx=dx)
+    dt = 0.4 * dx[0] / 5.8
+    k = 3
+    with R.Domain(n, dx=dx, order=2) as dom:
+        dom.set_state(U0)
+        dom.advance(dt, k)
+        Ug = dom.get_state()
+    for lo in _sample_boxes(n, 48, 5, seed=3) + [(80, 480)]:
+        hi = (lo[0] + 48, lo[1] + 48)
+        ref, gsl = _patch_oracle(U0, lo, hi, n, k, dt, dx, "clamp", order=2)
+        assert relerr(Ug[gsl], ref) <= 1e-12, lo
+
+
+def test_full_size_sampled_flux_difference_fd8k():
+    """f2 at the Table 4 8k^2 fp32 pad-1 size (tiled kernel): sampled rows of R vs the oracle."""
+    n = (8192, 8192)
+    dx = [1.0 / 8192] * 2
+    U0 = W.shock_bubble(n, dx=dx).astype(np.float32)
+    dt = 1e-5
+    with R.Domain(n, pad=1, dtype="f32", dx=dx) as dom:
+        dom.set_state(U0)
+        dom.flux_difference(dt)
+        Rg = dom.get_flux_difference()
+    for y0 in [0, 1, 4095, 8190]:
+        sub = np.ascontiguousarray(U0[max(0, y0 - 1):y0 + 3])   # rows y0-1 .. y0+2
+        g = oracle.Grid((8192, sub.shape[0]), pad=1, dx=dx)
+        Ro = oracle.flux_difference(g, sub, dt)
+        # rows whose y-neighbours are inside the sub-box (or are true boundary rows)
+        for r in range(sub.shape[0]):
+            gy = max(0, y0 - 1) + r
+            inner = (r > 0 or gy == 0) and (r < sub.shape[0] - 1 or gy == 8191)
+            if inner:
+                scale = np.max(np.abs(U0.astype(np.float64))) / dx[0] * 10
+                assert np.max(np.abs(Rg[gy].astype(np.float64) - Ro[r].astype(np.float64))) \
+                    <= 1e-4 * scale, gy
