@@ -33,12 +33,6 @@ template <typename T>  // tiled 2-D SoA form (TMA box {32+AL, C, fd_tile_rows, 1
 void launch_fluxdiff_tiled(const KArgs<T>& a, const void* tmap, cudaStream_t s);
 int fd_tile_rows(int elem);
 
-// 2-D variants whose kernel implements the device-side CFL step (k_step2d_pt)
-inline bool step2d_has_cfl(int variant) { return variant == 0 || (variant >= 30 && variant <= 39) || variant == 44 || variant == 46 ||
-         variant == 47 || (variant >= 80 && variant <= 84) ||
-         (variant >= 90 && variant <= 95); }
-
-int auto_rows_2d(const Geom& g);
 int auto_rows_3d(const Geom& g);
 
 }  // namespace rpl

@@ -134,8 +134,9 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
   ZState<T, V> zs;
   int bad = 0, nan = 0;
   const T qx = kc.q[0], nqx = kc.nq2[0], qy = kc.q[1], nqy = kc.nq2[1], qz = kc.q[2], nqz = kc.nq2[2];
-  T* dst_row = a.out + g.row(yr, z0 - 1) * g.rstride + (g.xo + xw + V * lane) * g.xstride;
-  const int64_t plane = g.rstride * g.P[1];
+  const int64_t plane = g.rstride * g.P[1], cs = g.cstride, xst = g.xstride;
+  // this lane's first output of plane z0 - 1 (advanced by one plane per store)
+  T* dst = a.out + g.row(yr, z0 - 1) * g.rstride + (g.xo + xw + V * lane) * xst;
 
   for (int kz = 0; kz < nplanes; ++kz) {
     const int z = z0 - 1 + kz;
@@ -238,14 +239,18 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
           for (int v = 0; v < V; ++v)
 #pragma unroll
             for (int c = 0; c < C; ++c) o[v][c] = zs.us[v][c] - (Pz[v][c] - zs.ph[v][c]);
-          T* dp = dst_row + (int64_t)(kz - 1) * plane;
+          dst += plane;  // plane z - 1
 #pragma unroll
           for (int v = 0; v < V; ++v) {
             if (out_ok[v] & row_out) {
               nan = max(nan, max(naninf(o[v][0]), naninf(o[v][C - 1])));
               if (ws) wmax = fmax(wmax, wavespeed<D>(o[v], gm1, gam));
+              T* p = dst + v * xst;
 #pragma unroll
-              for (int c = 0; c < C; ++c) dp[c * g.cstride + v * g.xstride] = o[v][c];
+              for (int c = 0; c < C; ++c) {
+                *p = o[v][c];
+                p += cs;
+              }
               const bool zf = (z - 1 < g.pad) | (z - 1 >= SZ - g.pad);
               if (xface[v] | yface | zf) {
                 if (g.img_fast)

@@ -432,7 +432,7 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
     int bw = 0, br = 0;
     const bool box = c->order == 2 ? tmap2d_box_o2(g, d->variant, &bw, &br)
                                    : tmap2d_box(g, d->variant, &bw, &br);
-    if (g.D == 2 && g.layout == 0 && box) {
+    if (g.D == 2 && g.layout == 0 && box) {  // every 2-D fused kernel is TMA-fed
       for (int p : d->local)
         for (int b = 0; b < 2; ++b)
           if (make_tmap(g, d->buf[b][p], d->tmap[b][p].b, bw, br) != 0)
@@ -977,8 +977,6 @@ extern "C" rpl_status rpl_advance_to(rpl_domain* d, double t_end, double cfl, in
   if (!d) return fail(RPL_E_INVALID_ARG, "null domain");
   if (!(cfl > 0.0) || !(t_end >= 0.0) || max_steps < 0)
     return fail(RPL_E_INVALID_ARG, "cfl > 0, t_end >= 0, max_steps >= 0 required");
-  if (d->g.D == 2 && use_fused(d) && d->cfg.order == 1 && !step2d_has_cfl(d->variant))
-    return fail(RPL_E_INVALID_ARG, "RPL_VARIANT %d has no device-side CFL step", d->variant);
   CU(cudaSetDevice(d->device));
   if (d->ghosts_stale) {
     rpl_status st = rpl_fill_padding(d);
