@@ -171,23 +171,39 @@ def cpu_baseline(wl, steps_cap=60, budget_s=12.0):
     n = list(wl["n"])
     if D == 3:  # bounded sample: a 128^3 sub-box of the same recipe
         n = [128, 128, 128]
+    elif n[0] * n[1] > 2048 * 2048:  # bounded sample: a 2048^2 sub-box
+        n = [2048, 2048]
     dx = [1.0 / wl["n"][0]] * D
     U = W.shock_bubble(tuple(n), dx=dx)
     if wl["dtype"] == "f32":
         U = U.astype(np.float32)
-    g = oracle.Grid(tuple(n), pad=2, dx=dx, order=wl.get("order", 1))
+    op = wl.get("op", "step")
+    g = oracle.Grid(tuple(n), pad=wl.get("pad", 2), dx=dx, order=wl.get("order", 1))
     dt = 0.4 * dx[0] / oracle.max_wavespeed(g, U.astype(np.float64))
+
+    def run(k):
+        if op == "fluxdiff":  # one flux-difference pass per "step" (Table 4 kernel)
+            for _ in range(k):
+                oracle.flux_difference(g, U, dt)
+        elif op == "cfl":  # the oracle's CFL loop (wavespeed pass + dt every step)
+            oracle.run_cfl(g, U, 1e9, cfl=0.9, n_reduced=0, max_steps=k)
+        else:
+            oracle.step(g, U, dt, k)
+
     t0 = time.perf_counter()
-    oracle.step(g, U, dt, 1)
+    run(1)
     one = time.perf_counter() - t0
     k = max(1, min(steps_cap, int(budget_s / max(one, 1e-6))))
     t0 = time.perf_counter()
-    oracle.step(g, U, dt, k)
+    run(k)
     el = time.perf_counter() - t0
     cells = int(np.prod(n))
-    return {"value": cells * k / el / 1e9, "unit": "Gcell-updates/s", "cores": 1,
+    unit = "Gcell/s" if op == "fluxdiff" else "Gcell-updates/s"
+    what = {"fluxdiff": "flux-difference passes", "cfl": "CFL steps"}.get(op, "steps")
+    return {"value": cells * k / el / 1e9, "unit": unit, "cores": 1,
             "kind": "oracle",
-            "sample": f"{'x'.join(map(str, n))} shock-bubble {wl['dtype']}, {k} steps, "
+            "sample": f"{'x'.join(map(str, n))} shock-bubble {wl['dtype']}"
+                      f"{' order 2' if wl.get('order', 1) == 2 else ''}, {k} {what}, "
                       f"plain-C oracle single thread ({el:.1f} s)"}
 
 
@@ -392,7 +408,11 @@ def main():
         t_total, _ = timed_loop(args.steps, profile=False)   # the headline timing
     wall = time.perf_counter() - wall0
     # the dominant kernel's own launch time for the roofline (separate, profiled pass)
-    _, (kern_ms, kern_launches) = timed_loop(max(5, min(args.steps, 20)), profile=True)
+    n_prof = max(5, min(args.steps, 20))
+    t_prof, (kern_ms, kern_launches) = timed_loop(n_prof, profile=True)
+    # exposed halo / synchronisation time per step: the step's event time minus its
+    # step-kernel time (pack/unpack, NCCL, P2P flag kernel, launch gaps)
+    exposed_ms = max(0.0, (t_prof * 1e3 - kern_ms) / n_prof)
     if world > 1:
         tt = torch.tensor([t_total], dtype=torch.float64,
                           device="cuda" if backend == "nccl" else "cpu")
@@ -452,7 +472,8 @@ def main():
     if wl.get("order", 1) == 2:
         kname = "k_step2d_o2" if (args.kernel == "fused" and D == 2) else "k_sweep2"
     if op == "fluxdiff":
-        kname = "k_fluxdiff"
+        kname = "k_fluxdiff_pt" if (args.kernel == "fused" and D == 2 and args.layout == "soa") \
+            else "k_fluxdiff"
     per_launch_ms = kern_ms / max(kern_launches, 1)
     launches_per_step_kernel = max(1, kern_launches // max(5, min(args.steps, 20)))
     if args.kernel == "split" or D != 2:
@@ -488,6 +509,10 @@ def main():
                        if op == "cfl" else None,
                        "paper_v100_ms": wl.get("paper_ms")},
             "roofline": roof, "gpu_launches": launches_per_step * args.steps,
+            "halo": {"exposed_ms_per_step": exposed_ms if op == "step" else None,
+                     "how": "per-step event time minus the step kernels' own event time "
+                            "(profiled pass): halo pack/unpack, NCCL or P2P flag sync and "
+                            "launch gaps; at N=1 only the launch gap + profiling events"},
             "clocks": clk.summary()}
     if e2e:
         line["e2e"] = e2e

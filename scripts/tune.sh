@@ -5,7 +5,8 @@ OUT=gpurun_out/$TAG
 mkdir -p $OUT
 for spec in "$@"; do
   IFS=: read -r w v extra <<< "$spec"
-  RPL_VARIANT=$v timeout 300 python bench.py --workload $w --steps 30 --no-cpu-baseline --e2e-steps 0 $extra > $OUT/b_${w}_v${v}.json 2>>$OUT/err.log
+  tag=$(echo "$extra" | tr -c 'a-z0-9' '_' | sed 's/_*$//')
+  RPL_VARIANT=$v timeout 300 python bench.py --workload $w --steps 30 --no-cpu-baseline --e2e-steps 0 $extra > $OUT/b_${w}_v${v}${tag:+_$tag}.json 2>>$OUT/err.log
 done
 OUT=$OUT python - <<'PY' > $OUT/summary.txt
 import json,glob,os
