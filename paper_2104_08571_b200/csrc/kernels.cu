@@ -10,8 +10,9 @@
 //                      then_reduce(Max)).
 //   k_fluxdiff[_pt]    the sec. 7.3 flux difference (Table 4; f2).
 // (Slower 2-D designs measured in round 1 -- per-warp row march, column march,
-// point-to-point hand-offs, low-register, warp march -- are described in
-// DESIGN.md's tuning log; their code is in git history, commit dcd05af.)
+// point-to-point hand-offs, low-register, warp march, software-pipelined -- are
+// described in DESIGN.md's tuning log; their code is in git history, commits
+// dcd05af and 289ce7f.)
 // All step kernels write the ghost images of the cells they produce (scheme.cuh),
 // so no separate boundary or halo kernel runs between steps on one rank.
 #include <cuda.h>
@@ -422,215 +423,6 @@ __global__ void __launch_bounds__(32 * NW, MB)
   if (ws) publish_max(a, wmax);
 }
 
-// ---------------------------------------------------------------------------
-// K-B (2-D), software-pipelined form of k_step2d_pt (V = 1): one CTA barrier per
-// tile instead of two.  Phase A(i) is one straight-line block holding two
-// independent chains -- the y-face of tile i (neighbour row's (U*, F_y) from
-// smem, own row's kept in registers) and the x-sweep of tile i+1 (from the TMA
-// stage) -- so the scheduler interleaves them (ILP 2).  After the barrier,
-// phase B(i) updates and stores tile i.  (U*, F_y) and y-face buffers are
-// double-buffered by tile parity.  Same arithmetic as k_step2d_pt: bitwise
-// identical results.
-// ---------------------------------------------------------------------------
-template <typename T, int NW>
-struct SmemSP {
-  static constexpr int W = 32, C = 4;
-  static constexpr int AL = 16 / (int)sizeof(T);
-  static constexpr int WB = W + AL;
-  static constexpr int STAGE = NW * C * WB;
-  static constexpr int XY = NW * 2 * C * W;
-  static constexpr int FY = NW * C * W;
-  static constexpr size_t bytes() { return (size_t)(2 * STAGE + 2 * XY + 2 * FY) * sizeof(T) + 64; }
-};
-
-template <typename T, int NW, int MB>
-__global__ void __launch_bounds__(32 * NW, MB)
-    k_step2d_sp(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
-                int nwin, int ntiles) {
-  constexpr int D = 2, C = 4, W = 32;
-  using SM = SmemSP<T, NW>;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  T* stage = reinterpret_cast<T*>(smem);
-  T* xy = stage + 2 * SM::STAGE;
-  T* fy = xy + 2 * SM::XY;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(fy + 2 * SM::FY);
-  const Geom& g = a.g;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int SX = (int)g.S[0], SY = (int)g.S[1];
-  const int G = gridDim.x;
-  Coef<T> kc;
-  if (!step_coef(a, kc)) return;
-  const bool ws = a.cf.dev != nullptr;
-  const T gam = (T)a.cf.gamma;
-  T wmax = T(0);
-  const T gm1 = a.gm1;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  const int nyb = ntiles / nwin;
-  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
-  // producer cursor (thread 0): tile index of the next issue
-  auto issue = [&](int i) {
-    const int tile = blockIdx.x + i * G;
-    if (tile >= ntiles) return;
-    const int s = i & 1;
-    const int w = tile % nwin, yb = tile / nwin;
-    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
-    const int x0 = (int)g.xo + w * (W - 2) - 1;
-    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
-                 (int)g.off[1] + yb * (NW - 2) - 1, 0);
-  };
-  if (threadIdx.x == 0) {
-    issue(0);
-    issue(1);
-  }
-  int bad = 0, nan = 0;
-  const int64_t cs = g.cstride;
-  // x-sweep of the tile at (win, yb) from stage s: U*, F_y of this warp's row
-  auto xsweep = [&](int s, int win, int yb, T* S_, T* G_) {
-    const int xw = win * (W - 2) - 1;
-    const int yr = yb * (NW - 2) - 1 + warp;
-    const int xv = xw + lane;
-    const bool row_in = (yr <= SY) & (yb < nyb);
-    const int sh = ((int)g.xo + xw) % SM::AL;
-    const T* st = stage + s * SM::STAGE + warp * C * SM::WB + sh + lane;
-    T U[C], F[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) U[c] = st[c * SM::WB];
-    const int b0 = phys_flux<D, 0>(U, F, gm1);
-    bad |= ((xv >= -1) & (xv <= SX) & row_in) ? b0 : 0;
-    T Pnx[C], Un[C], Fn[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      Un[c] = __shfl_down_sync(kFull, U[c], 1);
-      Fn[c] = __shfl_down_sync(kFull, F[c], 1);
-    }
-    force_face<D, 0>(U, F, Un, Fn, Pnx, kc.q[0], kc.nq2[0], gm1);
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      const T Ppv = __shfl_up_sync(kFull, Pnx[c], 1);
-      S_[c] = U[c] - (Pnx[c] - Ppv);
-    }
-    const int b1 = phys_flux<D, 1>(S_, G_, gm1);
-    bad |= ((lane >= 1) & (lane <= W - 2) & (xv < SX) & row_in) ? b1 : 0;
-  };
-  auto publish = [&](int par, const T* S_, const T* G_) {
-    T* xr = xy + par * SM::XY + warp * 2 * C * W + lane;
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      xr[c * W] = S_[c];
-      xr[(C + c) * W] = G_[c];
-    }
-  };
-  // ---- prologue: x-sweep of tile 0
-  int win = (int)blockIdx.x % nwin, yb = (int)blockIdx.x / nwin;
-  if (yb >= nyb) return;  // (block-uniform: every CTA of the grid has >= 1 tile)
-  T S_[C], G_[C];
-  mbar_wait(&bar[0], 0);
-  xsweep(0, win, yb, S_, G_);
-  publish(0, S_, G_);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    fence_proxy_async();
-    issue(2);
-  }
-  for (int i = 0;; ++i) {
-    // next tile (i + 1)
-    int wn = win + Gr, ybn = yb + Gq;
-    if (wn >= nwin) {
-      wn -= nwin;
-      ++ybn;
-    }
-    const bool has_next = ybn < nyb;
-    const int par = i & 1;
-    // ---- A(i): y-face of tile i  ||  x-sweep of tile i+1
-    if (has_next) mbar_wait(&bar[(i + 1) & 1], ((i + 1) >> 1) & 1);
-    T Sn[C], Gn[C], Py[C];
-    {
-      // neighbour row (warp - 1) of tile i; warp 0 reads its own row (result unused)
-      const T* pr = xy + par * SM::XY + (warp > 0 ? warp - 1 : 0) * 2 * C * W + lane;
-      T Sp[C], Gp[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        Sp[c] = pr[c * W];
-        Gp[c] = pr[(C + c) * W];
-      }
-      xsweep((i + 1) & 1, wn, ybn, Sn, Gn);  // stage holds zeros past the last tile
-      force_face<D, 1>(Sp, Gp, S_, G_, Py, kc.q[1], kc.nq2[1], gm1);
-    }
-    if (warp >= 1) {
-      T* fw = fy + par * SM::FY + warp * C * W + lane;  // face below row `warp`
-#pragma unroll
-      for (int c = 0; c < C; ++c) fw[c * W] = Py[c];
-    }
-    if (has_next) publish(par ^ 1, Sn, Gn);
-    __syncthreads();  // stage (i+1) consumed; faces of tile i and (U*, F_y) of tile i+1 published
-    if (threadIdx.x == 0) {
-      fence_proxy_async();
-      issue(i + 3);
-    }
-    // ---- B(i): update + store tile i
-    {
-      const int xw = win * (W - 2) - 1;
-      const int yr = yb * (NW - 2) - 1 + warp;
-      const int xv = xw + lane;
-      if ((warp >= 1) & (warp <= NW - 2) & (yr < SY) & (lane >= 1) & (lane <= W - 2) & (xv < SX)) {
-        const T* fu = fy + par * SM::FY + (warp + 1) * C * W + lane;  // face above
-        T o[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) o[c] = S_[c] - (fu[c * W] - Py[c]);
-        T* dst = a.out + ((int64_t)((int)g.off[1] + yr) * g.rstride + (int)g.xo + xv);
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          *dst = o[c];
-          dst += cs;
-        }
-        nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
-        if (ws) wmax = fmax(wmax, wavespeed<D>(o, gm1, gam));
-        if ((yr < g.pad) | (yr >= SY - g.pad) | (xv < g.pad) | (xv >= SX - g.pad))
-          images<D, 0>(a, xv, yr, 0, o);
-      }
-    }
-    if (!has_next) break;
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      S_[c] = Sn[c];
-      G_[c] = Gn[c];
-    }
-    win = wn;
-    yb = ybn;
-  }
-  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
-  if (ws) publish_max(a, wmax);
-}
-
-template <typename T, int NW, int MB>
-static void launch_sp2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
-  constexpr int W = 32;
-  using SM = SmemSP<T, NW>;
-  const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
-  const int nyb = (int)((a.g.S[1] + (NW - 2) - 1) / (NW - 2));
-  const int ntiles = nwin * nyb;
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaFuncSetAttribute(k_step2d_sp<T, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)SM::bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step2d_sp<T, NW, MB>, 32 * NW,
-                                                  SM::bytes());
-    if (per_sm < 1) per_sm = 1;
-  }
-  int nsm = 148, dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  int grid = per_sm * nsm;
-  if (grid > ntiles) grid = ntiles;
-  k_step2d_sp<T, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
-      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
-}
-
 template <typename T, int V, int NW, int MB = (V == 1 ? 2 : 1)>
 static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   constexpr int W = 32 * V;
@@ -906,10 +698,6 @@ int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
     case 44: nw = 24; break;
     case 46: nw = 14; break;
     case 47: nw = 20; break;
-    case 50: case 53: nw = 8; break;
-    case 51: nw = 16; break;
-    case 52: case 55: nw = 12; break;
-    case 54: case 56: nw = 10; break;
     default: nw = 12; break;  // 0, 37, 39
   }
   *box_w = 32 * v + al;
@@ -1076,13 +864,6 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 44: return launch_pt2d<T, 1, 24, 1>(a, tmap, s);
     case 46: return launch_pt2d<T, 1, 14, 2>(a, tmap, s);
     case 47: return launch_pt2d<T, 1, 20, 1>(a, tmap, s);
-    case 50: return launch_sp2d<T, 8, 2>(a, tmap, s);
-    case 51: return launch_sp2d<T, 16, 1>(a, tmap, s);
-    case 52: return launch_sp2d<T, 12, 1>(a, tmap, s);
-    case 53: return launch_sp2d<T, 8, 3>(a, tmap, s);
-    case 54: return launch_sp2d<T, 10, 2>(a, tmap, s);
-    case 55: return launch_sp2d<T, 12, 2>(a, tmap, s);
-    case 56: return launch_sp2d<T, 10, 3>(a, tmap, s);
     default: return launch_pt2d<T, 1, 12, 2>(a, tmap, s);  // 0 / 37: the default
   }
 }
