@@ -88,27 +88,65 @@ def decomposition(wl, nranks):
 
 
 class Clocks:
-    """Sample nvidia-smi clocks / throttle reasons during the timed region."""
+    """Sample SM clocks and clock-event (throttle) reasons during the timed region:
+    NVML polled every ~2 ms (the timed region of a short run lasts milliseconds),
+    nvidia-smi every 100 ms as the fallback."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clock-event reason bits
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40}
 
     def __init__(self, index):
         self.index = index
-        self.samples = []
+        self.samples = []   # (sm_mhz, max_mhz, set(reasons))
+        self.source = None
         self._stop = threading.Event()
         self._t = None
+        self._nv = None
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        props = torch.cuda.get_device_properties(self.index)
+        for i in range(pynvml.nvmlDeviceGetCount()):
+            h = pynvml.nvmlDeviceGetHandleByIndex(i)
+            pci = pynvml.nvmlDeviceGetPciInfo(h)
+            if pci.bus == props.pci_bus_id and pci.device == props.pci_device_id:
+                return pynvml, h
+        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def _run(self):
+        try:
+            nv, h = self._nvml_handle()
+            get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.source = "nvml"
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = get_r(h)
+                self.samples.append((float(sm), float(mx),
+                                     {k for k, bit in self.BITS.items() if r & bit}))
+                self._stop.wait(0.002)
+            return
+        except Exception:
+            self.samples = []
+        self.source = "nvidia-smi"
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index),
                                       f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
                                      capture_output=True, text=True, timeout=5).stdout
                 f = [v.strip() for v in out.strip().split(",")]
-                if len(f) >= 7:
-                    self.samples.append(f)
+                if len(f) >= 7 and f[0].replace(".", "").isdigit():
+                    self.samples.append((float(f[0]), float(f[1]),
+                                         {names[i] for i in range(4)
+                                          if f[3 + i].lower() == "active"}))
             except Exception:
                 pass
             self._stop.wait(0.1)
@@ -116,6 +154,7 @@ class Clocks:
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.05)  # first samples before the timed region starts
         return self
 
     def __exit__(self, *a):
@@ -125,14 +164,10 @@ class Clocks:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if s[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted(set().union(*[s[2] for s in self.samples]))
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": reasons, "samples": len(self.samples), "source": self.source}
 
 
 def N_get_fd(dom, ptr):
