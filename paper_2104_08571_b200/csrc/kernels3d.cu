@@ -370,8 +370,10 @@ static int launch3(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
 template <typename T>
 int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   if (a.g.layout == 1) return launch3<T, 1, 14, 1, 1>(a, tmap, s);  // AoS (configs[4])
+  // V = 2 (two cells per lane) only for fp32 -- must match win3() / the TMA box
+  if constexpr (sizeof(T) == 4)
+    if (a.variant == 21) return launch3<T, 2, 14>(a, tmap, s);
   switch (a.variant) {
-    case 21: return launch3<T, 2, 14>(a, tmap, s);
     case 50: return launch3<T, 1, 30>(a, tmap, s);
     case 51: return launch3<T, 1, 22>(a, tmap, s);
     case 52: return launch3<T, 1, 14, 2>(a, tmap, s);

@@ -421,3 +421,20 @@ def test_full_size_sampled_flux_difference_fd8k():
                 scale = np.max(np.abs(U0.astype(np.float64))) / dx[0] * 10
                 assert np.max(np.abs(Rg[gy].astype(np.float64) - Ro[r].astype(np.float64))) \
                     <= 1e-4 * scale, gy
+
+
+@pytest.mark.parametrize("variant,dtype", [("21", "f32"), ("21", "f64"), ("51", "f64"),
+                                           ("51", "f32")])
+def test_3d_kernel_variants_bitwise(variant, dtype, monkeypatch):
+    """3-D fused variants (RPL_VARIANT: 21 = two cells per lane for fp32, the default
+    for fp64; 51 = 22-row tiles) give bitwise the split kernel's result (ragged
+    windows, tiles and z-chunks)."""
+    n = (70, 33, 20)
+    dx = [1.0 / 70] * 3
+    U0 = W.shock_bubble(n, dx=dx)
+    if dtype == "f32":
+        U0 = U0.astype(np.float32)
+    dt = 0.4 * dx[0] / 5.8
+    ref = run_gpu(U0, dt, 5, dtype=dtype, kernel="split", dx=dx, rows_per_chunk=7)
+    monkeypatch.setenv("RPL_VARIANT", variant)
+    assert np.array_equal(run_gpu(U0, dt, 5, dtype=dtype, dx=dx, rows_per_chunk=7), ref)
