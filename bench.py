@@ -52,6 +52,8 @@ WORKLOADS = {
     # order-2 reconstruction (MUSCL-Hancock + FORCE), configs[1] shape
     "o2_1024": dict(ndim=2, n=(1024, 1024), dtype="f64", scaling="weak", order=2,
                     label="2-D Euler SLIC (MUSCL-Hancock + FORCE, order 2) 1024x1024/GPU fp64"),
+    "o2_s256": dict(ndim=3, n=(256, 256, 256), dtype="f64", scaling="weak", order=2,
+                    label="3-D Euler SLIC (order 2) 256^3 fp64 (x-y pass + z pass)"),
     # CFL-adaptive steps (Listing 8 wavespeed -> max -> dt every step);
     # one bench "step" = one run of cfl_steps CFL steps (--cfl-loop device|host)
     "cfl1024": dict(ndim=2, n=(1024, 1024), dtype="f64", scaling="weak", op="cfl", cfl_steps=20,
@@ -505,7 +507,8 @@ def main():
     alg_bytes = 2 * C * elem * local_cells  # per step-kernel launch (one partition per rank)
     kname = {"fused": {1: "k_sweep", 2: "k_step2d_pt", 3: "k_step3d"}[D], "split": "k_sweep"}[args.kernel]
     if wl.get("order", 1) == 2:
-        kname = "k_step2d_o2" if (args.kernel == "fused" and D == 2) else "k_sweep2"
+        kname = {2: "k_step2d_o2", 3: "k_step2d_o2<3> (x-y) + k_sweep2 (z)"}.get(D, "k_sweep2") \
+            if (args.kernel == "fused" and args.layout == "soa") else "k_sweep2"
     if op == "fluxdiff":
         kname = "k_fluxdiff_pt" if (args.kernel == "fused" and D == 2 and args.layout == "soa") \
             else "k_fluxdiff"

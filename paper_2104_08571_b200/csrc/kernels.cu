@@ -462,9 +462,9 @@ static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
 //   Y2  rows 2..NW-2: y-face between rows j-1 and j, published;
 //   upd rows 2..NW-3: U^{n+1} = U* - (Phi_{j+1/2} - Phi_{j-1/2}), store + images.
 // ---------------------------------------------------------------------------
-template <typename T, int NW>
+template <typename T, int NW, int C_ = 4>
 struct SmemO2 {
-  static constexpr int W = 32, C = 4;
+  static constexpr int W = 32, C = C_;
   static constexpr int AL = 16 / (int)sizeof(T);
   static constexpr int WB = W + AL;
   static constexpr int STAGE = NW * C * WB;
@@ -474,12 +474,14 @@ struct SmemO2 {
   static constexpr size_t bytes() { return (size_t)(2 * STAGE + SX + BR + FY) * sizeof(T) + 64; }
 };
 
-template <typename T, int NW, int MB>
+// D = 3: the x- and y-sweeps of every z-plane (tiles over (window, row block,
+// plane)); the z-sweep of the step follows as a separate pass (k_sweep2).
+template <typename T, int D, int NW, int MB>
 __global__ void __launch_bounds__(32 * NW, MB)
     k_step2d_o2(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
-                int nwin, int ntiles) {
-  constexpr int D = 2, C = 4, W = 32;
-  using SM = SmemO2<T, NW>;
+                int nwin, int nyb, int ntiles) {
+  constexpr int C = D + 2, W = 32;
+  using SM = SmemO2<T, NW, C>;
   extern __shared__ __align__(1024) unsigned char smem[];
   T* stage = reinterpret_cast<T*>(smem);
   T* sx = stage + 2 * SM::STAGE;
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
   const int G = gridDim.x;
   Coef<T> kc;
   if (!step_coef(a, kc)) return;
-  const bool ws = a.cf.dev != nullptr;
+  const bool ws = a.cf.dev != nullptr && a.cf.last;
   const T gam = (T)a.cf.gamma;
   T wmax = T(0);
   const T gm1 = a.gm1;
@@ -506,11 +508,11 @@ __global__ void __launch_bounds__(32 * NW, MB)
     const int tile = blockIdx.x + i * G;
     if (tile >= ntiles) return;
     const int s = i & 1;
-    const int w = tile % nwin, yb = tile / nwin;
+    const int w = tile % nwin, r = tile / nwin, yb = r % nyb, zp = r / nyb;
     mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
     const int x0 = (int)g.xo + w * (W - 4) - 2;
     tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
-                 (int)g.off[1] + yb * (NW - 4) - 2, 0);
+                 (int)g.off[1] + yb * (NW - 4) - 2, (int)g.off[2] + zp);
   };
   if (threadIdx.x == 0) {
     issue(0);
@@ -520,10 +522,13 @@ __global__ void __launch_bounds__(32 * NW, MB)
   const bool lane_in = (lane >= 1) & (lane <= 30);   // has both x-neighbours
   const bool lane_out = (lane >= 2) & (lane <= 29);  // U* valid
   const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
-  int win = (int)blockIdx.x % nwin, yb = (int)blockIdx.x / nwin;
-  const int nyb = ntiles / nwin;
+  int win = (int)blockIdx.x % nwin, yq = (int)blockIdx.x / nwin;  // yq = z * nyb + yb
+  const int nyz = ntiles / nwin;
+  const int SZ = (int)g.S[2];
   for (int i = 0;; ++i) {
-    if (yb >= nyb) break;
+    if (yq >= nyz) break;
+    const int yb = D == 2 ? yq : yq % nyb;
+    const int zp = D == 2 ? 0 : yq / nyb;
     const int xw = win * (W - 4) - 2;
     const int yr = yb * (NW - 4) - 2 + warp;
     const int xv = xw + lane;
@@ -611,7 +616,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
       T o[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) o[c] = S_[c] - (fu[c * W] - Py[c]);
-      T* dst = a.out + ((int64_t)((int)g.off[1] + yr) * g.rstride + (int)g.xo + xv);
+      T* dst = a.out + (g.row(yr, zp) * g.rstride + (int)g.xo + xv);
       const int64_t cs = g.cstride;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
@@ -620,32 +625,33 @@ __global__ void __launch_bounds__(32 * NW, MB)
       }
       nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
       if (ws) wmax = fmax(wmax, wavespeed<D>(o, gm1, gam));
-      if ((yr < g.pad) | (yr >= SY - g.pad) | (xv < g.pad) | (xv >= SX - g.pad))
-        images<D, 0>(a, xv, yr, 0, o);
+      const bool zf = D == 3 && ((zp < g.pad) | (zp >= SZ - g.pad));
+      if ((yr < g.pad) | (yr >= SY - g.pad) | (xv < g.pad) | (xv >= SX - g.pad) | zf)
+        images<D, 0>(a, xv, yr, zp, o);
     }
     win += Gr;
-    yb += Gq;
+    yq += Gq;
     if (win >= nwin) {
       win -= nwin;
-      ++yb;
+      ++yq;
     }
   }
   if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
   if (ws) publish_max(a, wmax);
 }
 
-template <typename T, int NW, int MB>
+template <typename T, int NW, int MB, int D = 2>
 static void launch_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   constexpr int W = 32;
-  using SM = SmemO2<T, NW>;
+  using SM = SmemO2<T, NW, D + 2>;
   const int nwin = (int)((a.g.S[0] + (W - 4) - 1) / (W - 4));
   const int nyb = (int)((a.g.S[1] + (NW - 4) - 1) / (NW - 4));
-  const int ntiles = nwin * nyb;
+  const int ntiles = nwin * nyb * (D == 3 ? (int)a.g.S[2] : 1);
   static int per_sm = 0;
   if (!per_sm) {
-    cudaFuncSetAttribute(k_step2d_o2<T, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_step2d_o2<T, D, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)SM::bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step2d_o2<T, NW, MB>, 32 * NW,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step2d_o2<T, D, NW, MB>, 32 * NW,
                                                   SM::bytes());
     if (per_sm < 1) per_sm = 1;
   }
@@ -655,8 +661,8 @@ static void launch_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   int grid = per_sm * nsm;
   if (grid > ntiles) grid = ntiles;
-  k_step2d_o2<T, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
-      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
+  k_step2d_o2<T, D, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb, ntiles);
 }
 
 // order-2 variants (RPL_VARIANT; box rows = NW)
@@ -684,6 +690,90 @@ static void launch_step2d_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s
     default: return launch_o2<T, 16, 1>(a, tmap, s);
   }
 }
+
+// ---------------------------------------------------------------------------
+// Order 2, 3-D: the z-sweep as a march (SoA).  A thread owns one (x, y) column
+// and a chunk of ZC planes; it carries U(z), U(z+1), the evolved upper boundary
+// value of plane z and the face below plane z in registers, so every evolved
+// value and every z-face is computed once (k_sweep2 evaluates each three times).
+// Coalesced: a warp's threads hold consecutive x.  Same operations per cell and
+// face as k_sweep2 along z: bitwise identical.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(128, 1) k_zmarch2(const __grid_constant__ KArgs<T> a, int zc) {
+  constexpr int D = 3, C = 5;
+  const Geom& g = a.g;
+  const int SX = (int)g.S[0], SY = (int)g.S[1], SZ = (int)g.S[2];
+  Coef<T> k;
+  if (!step_coef(a, k)) return;
+  const bool ws = a.cf.dev != nullptr && a.cf.last;
+  const T gam = (T)a.cf.gamma;
+  const T q = k.q[2], nq2 = k.nq2[2], h2 = k.h2[2], gm1 = a.gm1;
+  T wmax = T(0);
+  int bad = 0, nan = 0;
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col < (int64_t)SX * SY) {
+    const int x = (int)(col % SX), y = (int)(col / SX);
+    const int z0 = blockIdx.y * zc, z1 = min(z0 + zc, SZ);
+    T U0[C], U1[C], Um[C], bR[C], FbR[C], Pp[C];
+    {
+      T Umm[C], bL[C], FbL[C], cR[C], FcR[C];
+      load_cell<D, 0>(g, a.in, x, y, z0 - 2, Umm);
+      load_cell<D, 0>(g, a.in, x, y, z0 - 1, Um);
+      load_cell<D, 0>(g, a.in, x, y, z0, U0);
+      load_cell<D, 0>(g, a.in, x, y, z0 + 1, U1);
+      bad |= hancock<D, 2>(Umm, Um, U0, h2, gm1, bL, FbL, cR, FcR);   // plane z0 - 1
+      bad |= hancock<D, 2>(Um, U0, U1, h2, gm1, bL, FbL, bR, FbR);    // plane z0
+      force_face<D, 2>(cR, FcR, bL, FbL, Pp, q, nq2, gm1);           // face z0 - 1/2
+    }
+    for (int z = z0; z < z1; ++z) {
+      T U2[C], bL[C], FbL[C], nR[C], FnR[C], P[C], o[C];
+      load_cell<D, 0>(g, a.in, x, y, z + 2, U2);
+      bad |= hancock<D, 2>(U0, U1, U2, h2, gm1, bL, FbL, nR, FnR);  // plane z + 1
+      force_face<D, 2>(bR, FbR, bL, FbL, P, q, nq2, gm1);           // face z + 1/2
+#pragma unroll
+      for (int c = 0; c < C; ++c) o[c] = U0[c] - (P[c] - Pp[c]);
+      nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
+      store_cell<D, 0>(g, a.out, x, y, z, o);
+      if (ws) wmax = fmax(wmax, wavespeed<D>(o, gm1, gam));
+      if (near_face<D>(g, x, y, z)) images<D, 0>(a, x, y, z, o);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Pp[c] = P[c];
+        bR[c] = nR[c];
+        FbR[c] = FnR[c];
+        U0[c] = U1[c];
+        U1[c] = U2[c];
+      }
+    }
+  }
+  if (bad < 0 || nan >= kExpMask<T>) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
+}
+
+template <typename T>
+void launch_zmarch2(const KArgs<T>& a, cudaStream_t s) {
+  const int64_t cols = a.g.S[0] * a.g.S[1];
+  const int bx = (int)((cols + 127) / 128);
+  // z-chunks: enough blocks for ~16 warps per SM, at least 16 planes per chunk
+  int nzc = (int)((148 * 4 + bx - 1) / bx);
+  const int SZ = (int)a.g.S[2];
+  if (nzc > SZ / 16) nzc = SZ / 16;
+  if (nzc < 1) nzc = 1;
+  const int zc = (SZ + nzc - 1) / nzc;
+  nzc = (SZ + zc - 1) / zc;
+  k_zmarch2<T><<<dim3(bx, nzc), 128, 0, s>>>(a, zc);
+}
+template void launch_zmarch2<float>(const KArgs<float>&, cudaStream_t);
+template void launch_zmarch2<double>(const KArgs<double>&, cudaStream_t);
+
+// order 2, 3-D: x/y sweeps of every plane in one pass (box {32+AL, C, 16, 1})
+template <typename T>
+void launch_xy3d_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  launch_o2<T, 16, 1, 3>(a, tmap, s);
+}
+template void launch_xy3d_o2<float>(const KArgs<float>&, const void*, cudaStream_t);
+template void launch_xy3d_o2<double>(const KArgs<double>&, const void*, cudaStream_t);
 
 int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
   const int al = 16 / g.elem;  // see SmemPT::AL

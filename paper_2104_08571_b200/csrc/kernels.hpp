@@ -19,7 +19,11 @@ int make_tmap3d(const Geom& g, const void* buf, void* map_out, int variant);
 // 4-D tensor map {pitch, C, P1, P2} of a SoA buffer with box {box_w, C, box_rows, 1}
 int make_tmap(const Geom& g, const void* buf, void* map_out, int box_w, int box_rows);
 int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows);
-int tmap2d_box_o2(const Geom& g, int variant, int* box_w, int* box_rows);  // order-2 kernel  // 0 if 2-D uses TMA  // 128-byte CUtensorMap
+int tmap2d_box_o2(const Geom& g, int variant, int* box_w, int* box_rows);  // order-2 kernel
+template <typename T>  // order 2, 3-D SoA: x/y sweeps of all planes (box {32+AL, C, 16, 1})
+void launch_xy3d_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s);
+template <typename T>  // order 2, 3-D SoA: the z-sweep as a per-column march
+void launch_zmarch2(const KArgs<T>& a, cudaStream_t s);  // 0 if 2-D uses TMA  // 128-byte CUtensorMap
 int window3d(const Geom& g);                                     // outputs per 3-D x-window
 template <typename T>
 void launch_fill(const Geom& g, int part, T* const* bufs, cudaStream_t s);

@@ -422,7 +422,10 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
     d->tmaps_ok = true;
     for (int p : d->local)
       for (int b = 0; b < 2; ++b) {
-        const int r = make_tmap3d(g, d->buf[b][p], d->tmap[b][p].b, d->variant);
+        // order 2 (SoA): the x/y-plane kernel's box {32+AL, C, 16, 1}
+        const int r = (c->order == 2 && g.layout == 0)
+                          ? make_tmap(g, d->buf[b][p], d->tmap[b][p].b, 32 + 16 / g.elem, 16)
+                          : make_tmap3d(g, d->buf[b][p], d->tmap[b][p].b, d->variant);
         if (r != 0) d->tmaps_ok = false;
       }
     if (!d->tmaps_ok && c->kernel == RPL_KERNEL_FUSED)
@@ -766,20 +769,27 @@ extern "C" rpl_status rpl_fill_padding(rpl_domain* d) {
 }
 
 static bool use_fused(const rpl_domain* d) {
-  if (d->cfg.order == 2)  // order 2: fused 2-D SoA kernel; 3-D and AoS run the split kernel
-    return d->cfg.kernel == RPL_KERNEL_FUSED && d->g.D == 2 && d->g.layout == 0;
+  if (d->cfg.order == 2)  // order 2: fused 2-D / fused x-y + z pass in 3-D (SoA); AoS splits
+    return d->cfg.kernel == RPL_KERNEL_FUSED && d->g.layout == 0 &&
+           (d->g.D == 2 || (d->g.D == 3 && d->tmaps_ok));
   return d->cfg.kernel == RPL_KERNEL_FUSED &&
          ((d->g.D == 2 && d->g.layout == 0) || (d->g.D == 3 && d->tmaps_ok));
 }
 
+// kernel passes per step: fused = 1 (3-D order 2: x-y pass + z pass), split = D
+static int passes(const rpl_domain* d) {
+  if (!use_fused(d)) return d->g.D;
+  return (d->g.D == 3 && d->cfg.order == 2) ? 2 : 1;
+}
+
 extern "C" rpl_status rpl_launches_per_step(const rpl_domain* d, int32_t* out) {
   if (!d || !out) return fail(RPL_E_INVALID_ARG, "null argument");
-  int n = (int)d->local.size() * (use_fused(d) ? 1 : d->g.D);
+  int n = (int)d->local.size() * passes(d);
   int ne = 0;
   for (auto& P : d->send_peers) ne += (int)P.edges.size();
   for (auto& P : d->recv_peers) ne += (int)P.edges.size();
-  n += ne * (use_fused(d) ? 1 : d->g.D);
-  if (d->p2p) n += use_fused(d) ? 1 : d->g.D;  // one flag kernel per exchange
+  n += ne * passes(d);
+  if (d->p2p) n += passes(d);  // one flag kernel per exchange
   *out = n;
   return RPL_OK;
 }
@@ -806,8 +816,9 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps, const CflArgs*
   a.order = d->cfg.order;
   if (cf) a.cf = *cf;
   const bool fused = use_fused(d);
+  const bool xyz = fused && g.D == 3 && d->cfg.order == 2;  // x-y pass, then z pass
   for (int s = 0; s < nsteps; ++s) {
-    const int nsweep = fused ? 1 : g.D;
+    const int nsweep = passes(d);
     if (cf) a.cf.step = cf->step + s;
     for (int sw = 0; sw < nsweep; ++sw) {
       const int nb = d->cur ^ 1;
@@ -821,7 +832,9 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps, const CflArgs*
         a.out = (T*)d->buf[nb][p];
         const bool prof = d->ev_used + 2 <= d->ev.size();
         if (prof) cudaEventRecord(d->ev[d->ev_used], d->stream);
-        if (fused && g.D == 2) launch_step2d<T>(a, d->tmap[d->cur][p].b, d->stream);
+        if (xyz && sw == 0) launch_xy3d_o2<T>(a, d->tmap[d->cur][p].b, d->stream);
+        else if (xyz) launch_zmarch2<T>(a, d->stream);
+        else if (fused && g.D == 2) launch_step2d<T>(a, d->tmap[d->cur][p].b, d->stream);
         else if (fused) launch_step3d<T>(a, d->tmap[d->cur][p].b, d->stream);
         else launch_sweep<T>(a, sw, d->stream);
         if (prof) {
@@ -937,7 +950,7 @@ static rpl_status advance_to_t(rpl_domain* d, const CflArgs& base, int max_steps
   CU(cudaGetLastError());
   rpl_status st = reduce_max(d, &d->d_cfl->S[0], 1);
   if (st) return st;
-  const int nsweep = use_fused(d) ? 1 : d->g.D;
+  const int nsweep = passes(d);
   const int cur0 = d->cur;
   int launched = 0, chunk = 8;
   double t_prev = 0.0;
