@@ -519,7 +519,8 @@ def main():
     else:
         alg_bytes_launch = alg_bytes
     achieved = alg_bytes_launch / (per_launch_ms / 1e3) / 1e9
-    traffic = ncu_traffic(f"{args.workload}_{args.kernel}")
+    traffic = ncu_traffic(f"{args.workload}_{wl['dtype']}_{args.layout}") \
+        if args.workload == "l256" else ncu_traffic(f"{args.workload}_{args.kernel}")
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
             "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json copy bandwidth, burst)",
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
