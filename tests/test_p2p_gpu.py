@@ -96,6 +96,18 @@ def test_p2p_device_cfl_bitwise_equal_single_rank(n, parts, kw):
     _check(n, parts, kw, 0.02)
 
 
+@pytest.mark.parametrize("n,parts,kw", [
+    ((130, 64), (1, 2), dict(order=2)),
+    ((40, 32, 24), (1, 2, 2), dict(order=2)),
+    ((40, 32, 24), (1, 1, 2), dict(order=2, kernel="split")),
+])
+def test_p2p_order2_bitwise_equal_single_rank(n, parts, kw):
+    """Order 2 (radius-2 halos; in 3-D two passes per step) over P2P ranks."""
+    _check(n, parts, kw, None)
+
+
+
+
 def _check(n, parts, kw, t_end):
     world = int(np.prod(parts))
     steps = 6
