@@ -438,3 +438,16 @@ def test_3d_kernel_variants_bitwise(variant, dtype, monkeypatch):
     ref = run_gpu(U0, dt, 5, dtype=dtype, kernel="split", dx=dx, rows_per_chunk=7)
     monkeypatch.setenv("RPL_VARIANT", variant)
     assert np.array_equal(run_gpu(U0, dt, 5, dtype=dtype, dx=dx, rows_per_chunk=7), ref)
+
+
+def test_configs1_full_field_100_steps():
+    """BASELINE configs[1] exactly as north_star states the bar: 2-D 1024^2 fp64, 100
+    steps on the GPU (bench launch configuration) vs the oracle over the whole field,
+    max relative error <= 1e-10 (reading S15 metric)."""
+    n = (1024, 1024)
+    dx = [1.0 / 1024] * 2
+    U0 = W.shock_bubble(n, dx=dx)
+    dt = 0.4 * dx[0] / oracle.max_wavespeed(oracle.Grid(n), U0)
+    Ug = run_gpu(U0, dt, 100, dx=dx)
+    Uo = run_oracle(U0, dt, 100, dx)
+    assert relerr(Ug, Uo) <= 1e-10
