@@ -144,3 +144,18 @@ def test_order2_config_checks():
     assert "RPL_E_PAD_TOO_SMALL" in str(e.value)
     with pytest.raises(N.RplError):
         R.config_check(size=(64, 32), pad=2, order=3)
+
+
+def test_plain_c_consumer(tmp_path):
+    """The boundary is a C ABI: a plain C program (tests/c/abi_host.c) compiled with gcc
+    against include/ripple_fv.h and linked to libripple_fv.so uses the host-only calls."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2104_08571_b200")
+    exe = str(tmp_path / "abi_host")
+    subprocess.check_call(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "tests", "c", "abi_host.c"), "-L", libdir,
+                           "-lripple_fv", f"-Wl,-rpath,{libdir}", "-o", exe])
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.strip() == "ok"
