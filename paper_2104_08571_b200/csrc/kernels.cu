@@ -668,10 +668,10 @@ static void launch_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
 // order-2 variants (RPL_VARIANT; box rows = NW)
 static int o2_rows(int variant) {
   switch (variant) {
+    case 70: return 16;
     case 71: return 12;
     case 72: return 12;
-    case 73: return 24;
-    default: return 16;
+    default: return 24;  // 0 / 73: the default (DESIGN.md tuning log)
   }
 }
 
@@ -684,10 +684,10 @@ int tmap2d_box_o2(const Geom& g, int variant, int* box_w, int* box_rows) {
 template <typename T>
 static void launch_step2d_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   switch (a.variant) {
+    case 70: return launch_o2<T, 16, 1>(a, tmap, s);
     case 71: return launch_o2<T, 12, 2>(a, tmap, s);
     case 72: return launch_o2<T, 12, 1>(a, tmap, s);
-    case 73: return launch_o2<T, 24, 1>(a, tmap, s);
-    default: return launch_o2<T, 16, 1>(a, tmap, s);
+    default: return launch_o2<T, 24, 1>(a, tmap, s);
   }
 }
 
