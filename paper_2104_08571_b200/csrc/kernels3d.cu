@@ -69,7 +69,7 @@ template <typename T, int V, int TY, int MB, int L>
 __global__ void __launch_bounds__(32 * (TY + 2), MB)
     k_step3d(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
              int nwin, int nyb) {
-  constexpr int D = 3, C = 5, W = 32 * V, R = TY + 2;
+  constexpr int D = 3, C = 5, W = 32 * V;
   using SM = Smem3<TY, V, T>;
   extern __shared__ __align__(1024) unsigned char smem[];
   T* stage = reinterpret_cast<T*>(smem);
