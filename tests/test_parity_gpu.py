@@ -451,3 +451,39 @@ def test_configs1_full_field_100_steps():
     Ug = run_gpu(U0, dt, 100, dx=dx)
     Uo = run_oracle(U0, dt, 100, dx)
     assert relerr(Ug, Uo) <= 1e-10
+
+
+@pytest.mark.parametrize("n", [(2,), (3,), (2, 2), (3, 2), (2, 5, 3), (2, 2, 2)])
+@pytest.mark.parametrize("bc", ["clamp", "periodic", "reflective"])
+@pytest.mark.parametrize("kernel", ["fused", "split"])
+def test_minimum_sizes(n, bc, kernel):
+    """Degenerate extents: every dim exactly pad (2) or just above -- the windows,
+    tiles and z-chunks are almost all halo, every cell is a boundary cell."""
+    D = len(n)
+    dx = [1.0 / 8] * D
+    U0 = W.random_state(n, seed=17)
+    dt = 0.2 * dx[0] / 3.0
+    kw = dict(bc_lo=[bc] * D, bc_hi=[bc] * D)
+    Ug = run_gpu(U0, dt, 4, dx=dx, kernel=kernel, **kw)
+    Uo = run_oracle(U0, dt, 4, dx, **kw)
+    assert relerr(Ug, Uo) <= 1e-10
+
+
+def test_zero_steps_and_repeated_calls_compose():
+    """advance(dt, 0) is a no-op; advance(dt, 3) == three advance(dt, 1) calls (bitwise)."""
+    n = (70, 40)
+    dx = [1.0 / 70] * 2
+    U0 = W.shock_bubble(n, dx=dx)
+    dt = 0.4 * dx[0] / 5.8
+    with R.Domain(n, dx=dx) as dom:
+        dom.set_state(U0)
+        dom.advance(dt, 0)
+        assert np.array_equal(dom.get_state(), U0)
+        dom.advance(dt, 3)
+        a = dom.get_state()
+    with R.Domain(n, dx=dx) as dom:
+        dom.set_state(U0)
+        for _ in range(3):
+            dom.advance(dt, 1)
+        b = dom.get_state()
+    assert np.array_equal(a, b)
