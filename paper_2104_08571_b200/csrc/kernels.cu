@@ -233,6 +233,12 @@ __global__ void __launch_bounds__(32 * NW, MB)
     issue(1);
   }
   int bad = 0, nan = 0;
+  // loop-invariant addresses (hoisted by hand: the asm barriers/TMA calls in the
+  // loop would otherwise make the compiler recompute them every tile)
+  const unsigned bar_a0 = smem_u32(&bar[0]), bar_a1 = smem_u32(&bar[1]);
+  const T* const st_lane = stage + warp * C * SM::WB + V * lane;
+  T* const xr_lane = xy + warp * 2 * C * W + V * lane;
+  T* const out_lane = a.out + (int64_t)g.xo + V * lane;
   // tile t = blockIdx.x + i G  <->  (win, yb) = (t % nwin, t / nwin), advanced
   // incrementally (no per-tile integer division)
   const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
@@ -246,12 +252,12 @@ __global__ void __launch_bounds__(32 * NW, MB)
     const bool row_in = yr <= SY;
     const bool row_out = (warp >= 1) & (warp <= NW - 2) & (yr < SY);
     const int s = i & 1;
-    mbar_wait(&bar[s], (i >> 1) & 1);
+    mbar_wait_u32(s ? bar_a1 : bar_a0, (i >> 1) & 1);
     // ---- X
     T U[V][C], F[V][C], S_[V][C], G_[V][C];
     {
       const int sh = ((int)g.xo + xw) % SM::AL;
-      const T* st = stage + s * SM::STAGE + warp * C * SM::WB + sh + V * lane;
+      const T* st = st_lane + s * SM::STAGE + sh;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         const VT u = *reinterpret_cast<const VT*>(st + c * SM::WB);
@@ -297,7 +303,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
       bad |= ((slot >= 1) & (slot <= W - 2) & (xv < SX) & row_in) ? b : 0;
     }
     {
-      T* xr = xy + warp * 2 * C * W + V * lane;
+      T* xr = xr_lane;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         VT sv, gv;
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
     __syncthreads();  // (B) y-faces published
     // ---- update + store
     if (row_out) {
-      T* dst = a.out + ((int64_t)((int)g.off[1] + yr) * g.rstride + (int)g.xo + xw + V * lane);
+      T* dst = out_lane + ((int64_t)((int)g.off[1] + yr) * g.rstride + xw);
       const T* fu = fy + warp * C * W + V * lane;
       T o[V][C];
 #pragma unroll
