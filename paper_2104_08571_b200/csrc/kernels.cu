@@ -20,6 +20,7 @@
 #include <stdint.h>
 
 #include "async.cuh"
+#include "launch.cuh"
 #include "kernels.hpp"
 #include "scheme.cuh"
 
@@ -436,18 +437,9 @@ static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((a.g.S[1] + (NW - 2) - 1) / (NW - 2));
   const int ntiles = nwin * nyb;
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaFuncSetAttribute(k_step2d_pt<T, V, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)SM::bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step2d_pt<T, V, NW, MB>, 32 * NW,
-                                                  SM::bytes());
-    if (per_sm < 1) per_sm = 1;
-  }
-  int nsm = 148;
-  int dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  static int cache[kMaxDevices] = {0};
+  const int per_sm = resident_ctas(k_step2d_pt<T, V, NW, MB>, 32 * NW, SM::bytes(), cache);
+  const int nsm = sm_count();
   int grid = per_sm * nsm;
   if (grid > ntiles) grid = ntiles;
   k_step2d_pt<T, V, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
@@ -653,18 +645,9 @@ static void launch_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   const int nwin = (int)((a.g.S[0] + (W - 4) - 1) / (W - 4));
   const int nyb = (int)((a.g.S[1] + (NW - 4) - 1) / (NW - 4));
   const int ntiles = nwin * nyb * (D == 3 ? (int)a.g.S[2] : 1);
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaFuncSetAttribute(k_step2d_o2<T, D, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)SM::bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step2d_o2<T, D, NW, MB>, 32 * NW,
-                                                  SM::bytes());
-    if (per_sm < 1) per_sm = 1;
-  }
-  int nsm = 148;
-  int dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  static int cache[kMaxDevices] = {0};
+  const int per_sm = resident_ctas(k_step2d_o2<T, D, NW, MB>, 32 * NW, SM::bytes(), cache);
+  const int nsm = sm_count();
   int grid = per_sm * nsm;
   if (grid > ntiles) grid = ntiles;
   k_step2d_o2<T, D, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
@@ -1205,17 +1188,9 @@ static void launch_fd_pt(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((a.g.S[1] + (NW - 2) - 1) / (NW - 2));
   const int ntiles = nwin * nyb;
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaFuncSetAttribute(k_fluxdiff_pt<T, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)SM::bytes());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fluxdiff_pt<T, NW, MB>, 32 * NW,
-                                                  SM::bytes());
-    if (per_sm < 1) per_sm = 1;
-  }
-  int nsm = 148, dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  static int cache[kMaxDevices] = {0};
+  const int per_sm = resident_ctas(k_fluxdiff_pt<T, NW, MB>, 32 * NW, SM::bytes(), cache);
+  const int nsm = sm_count();
   int grid = per_sm * nsm;
   if (grid > ntiles) grid = ntiles;
   k_fluxdiff_pt<T, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(

@@ -25,6 +25,7 @@
 #include <stdlib.h>
 
 #include "async.cuh"
+#include "launch.cuh"
 #include "kernels.hpp"
 #include "scheme.cuh"
 
@@ -356,12 +357,8 @@ static int launch3(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   const int nyb = (int)((g.S[1] + TY - 1) / TY);
   const int nzc = (int)((g.S[2] + a.rows - 1) / a.rows);
   const size_t sm = Smem3<TY, V, T>::bytes();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_step3d<T, V, TY, MB, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sm);
-    attr = true;
-  }
+  static int cache[kMaxDevices] = {0};
+  resident_ctas(k_step3d<T, V, TY, MB, L>, 32 * (TY + 2), sm, cache);  // sets the smem attribute
   k_step3d<T, V, TY, MB, L><<<nwin * nyb * nzc, 32 * (TY + 2), sm, s>>>(
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb);
   return 0;
