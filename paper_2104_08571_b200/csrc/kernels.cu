@@ -689,7 +689,7 @@ static void launch_step2d_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s
 // face as k_sweep2 along z: bitwise identical.
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(128, 1) k_zmarch2(const __grid_constant__ KArgs<T> a, int zc) {
+__global__ void __launch_bounds__(128, 3) k_zmarch2(const __grid_constant__ KArgs<T> a, int zc) {
   constexpr int D = 3, C = 5;
   const Geom& g = a.g;
   const int SX = (int)g.S[0], SY = (int)g.S[1], SZ = (int)g.S[2];
@@ -744,8 +744,10 @@ template <typename T>
 void launch_zmarch2(const KArgs<T>& a, cudaStream_t s) {
   const int64_t cols = a.g.S[0] * a.g.S[1];
   const int bx = (int)((cols + 127) / 128);
-  // z-chunks: enough blocks for ~16 warps per SM, at least 16 planes per chunk
-  int nzc = (int)((148 * 4 + bx - 1) / bx);
+  // z-chunks: about 8 waves of resident blocks (short tail), at least 16 planes each
+  static int cache[kMaxDevices] = {0};
+  const int slots = resident_ctas(k_zmarch2<T>, 128, 0, cache) * sm_count();
+  int nzc = (int)((8LL * slots + bx - 1) / bx);
   const int SZ = (int)a.g.S[2];
   if (nzc > SZ / 16) nzc = SZ / 16;
   if (nzc < 1) nzc = 1;

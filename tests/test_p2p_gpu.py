@@ -106,6 +106,15 @@ def test_p2p_order2_bitwise_equal_single_rank(n, parts, kw):
     _check(n, parts, kw, None)
 
 
+@pytest.mark.parametrize("n,parts,kw", [
+    ((128, 96), (1, 8), {}),
+    ((40, 32, 24), (2, 2, 2), dict(dtype="f32")),
+])
+def test_p2p_eight_ranks_bitwise_equal_single_rank(n, parts, kw):
+    """8 ranks (the north star's largest GPU count), y-slabs and a 2x2x2 block grid."""
+    _check(n, parts, kw, None)
+
+
 
 
 def _check(n, parts, kw, t_end):
