@@ -332,7 +332,12 @@ def main():
     # RPL_SHARE_DEVICE=1: every rank on cuda:0 (functional check of the N>1 path on
     # a 1-GPU box; timings are then meaningless: the processes time-slice one GPU)
     share = os.environ.get("RPL_SHARE_DEVICE") == "1"
-    backend = "nccl" if args.transport == "nccl" else "gloo"  # P2P: host coordination only
+    # torch.distributed over NCCL for the plumbing (ncclUniqueId broadcast, IPC-handle
+    # all-gather, max-over-ranks timing); gloo only when all ranks share one GPU
+    # (NCCL rejects two ranks on one device)
+    backend = "gloo" if share else "nccl"
+    if share and args.transport == "nccl":
+        raise SystemExit("RPL_SHARE_DEVICE=1 needs --transport p2p (NCCL: one rank per GPU)")
     if world > 1:
         torch.cuda.set_device(0 if share else local_rank)
         if backend == "nccl":
