@@ -532,6 +532,20 @@ def main():
             "alg_bytes_per_launch": alg_bytes_launch, "launch_ms": per_launch_ms,
             "launches_per_step": launches_per_step_kernel,
             "frac_of_8TBs": achieved / 8000.0}
+    if op == "step" and wl.get("order", 1) == 1:
+        # the second ceiling of this path: floating-point issue.  Algorithmic FP
+        # instructions per cell-step of the scheme as written in scheme.cuh (DESIGN.md
+        # §6: 2-D 132, 3-D 240, 1-D 52; no tile recompute) against the measured issue
+        # rate of tools/dp_microbench.cu (fp64 57.4, fp32 122.1 lanes/clk/SM at
+        # 1.965 GHz on 148 SMs).
+        ops = {1: 52, 2: 132, 3: 240}[D]
+        lanes = 57.41 if elem == 8 else 122.11
+        peak_g = lanes * 148 * 1.965
+        ach_g = ops * local_cells / (per_launch_ms / 1e3) / 1e9 / \
+            (D if args.kernel == "split" else 1)
+        roof["fp_issue"] = {"ops_per_cell": ops, "achieved_gops": ach_g, "peak_gops": peak_g,
+                            "frac": ach_g / peak_g,
+                            "peak_source": "profiles/r1/dp_microbench.txt (measured)"}
     vs = None
     if op == "fluxdiff" and wl.get("paper_ms"):
         # paper Table 4 (V100, strided) time for the same pass: context, other hardware
