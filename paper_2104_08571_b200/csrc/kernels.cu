@@ -917,13 +917,17 @@ void launch_sweep(const KArgs<T>& a, int d, cudaStream_t s) {
 
 
 int auto_rows_3d(const Geom& g) {
-  // z-planes per CTA: enough CTAs for ~6 waves of 148, at least 8 planes per march
+  // z-planes per CTA: 8-10 z-chunks (about 24 CTAs per SM), at least 16 planes per
+  // march (each chunk recomputes 2 planes).  Measured (profiles/r1/rows_sweep.txt):
+  // 384^3 fp32 39 planes 1088 us vs 128 planes 1270 us; 512^3 fp64 64 planes
+  // 4535 us vs 256 planes 4834 us; 256^3 fp64 32 planes 705 us vs 43 planes 716 us.
   const int64_t ww = window3d(g);
   const int64_t tiles = ((g.S[0] + ww - 1) / ww) * ((g.S[1] + 13) / 14);  // (TY = 14 estimate)
-  int64_t nzc = (148 * 6 + tiles - 1) / tiles;
-  if (nzc < 1) nzc = 1;
+  int64_t nzc = (148 * 24 + tiles - 1) / tiles;
+  if (nzc < 8) nzc = 8;
+  if (nzc > 10) nzc = 10;
   int64_t rows = (g.S[2] + nzc - 1) / nzc;
-  if (rows < 8) rows = 8;
+  if (rows < 16) rows = 16;
   if (rows > g.S[2]) rows = g.S[2];
   return (int)rows;
 }

@@ -27,6 +27,7 @@
 #include "async.cuh"
 #include "launch.cuh"
 #include "kernels.hpp"
+#include "packed.cuh"
 #include "scheme.cuh"
 
 namespace rpl {
@@ -281,6 +282,231 @@ __global__ void __launch_bounds__(32 * (TY + 2), MB)
   if (ws) publish_max(a, wmax);
 }
 
+
+// ------------------------------------------------------------------------
+// fp32, SoA: the same fused x-y-z pass with two tile rows per lane, packed
+// (packed.cuh: FFMA2/FADD2 do both rows' arithmetic in one instruction).
+// Warp w owns tile rows j0 = w and j1 = w + NW (R = 2 NW rows, TY = R - 2
+// outputs, rows 0 and R-1 are the y-halo).  Every per-cell operation is the
+// scalar kernel's, so the result is bitwise that of k_step3d / k_sweep.
+// ------------------------------------------------------------------------
+template <int NW>
+struct SmemRP {
+  static constexpr int W = 32, R = 2 * NW, C = 5, NS = 2;
+  static constexpr int AL = 4;                      // 16-byte TMA alignment in floats
+  static constexpr int WB = W + AL;
+  static constexpr int STAGE = R * C * WB;          // floats per ring stage
+  static constexpr int XY = R * 2 * C * W;          // (U*, F_y) per tile row
+  static constexpr int FY = (R - 1) * C * W;        // y-faces
+  static constexpr size_t bytes() { return (size_t)(NS * STAGE + XY + FY) * 4 + 64; }
+};
+
+template <int NW, int MB>
+__global__ void __launch_bounds__(32 * NW, MB)
+    k_step3d_rp(const __grid_constant__ KArgs<float> a, const __grid_constant__ CUtensorMap tmap,
+                int nwin, int nyb) {
+  constexpr int D = 3, C = 5, W = 32, R = 2 * NW, TY = R - 2;
+  using SM = SmemRP<NW>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  float* stage = reinterpret_cast<float*>(smem);
+  float* xy = stage + SM::NS * SM::STAGE;
+  float* fyb = xy + SM::XY;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + SM::FY);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int t = blockIdx.x;
+  const int win = t % nwin;
+  t /= nwin;
+  const int yb = t % nyb;
+  const int zc = t / nyb;
+  const int xw = win * (W - 2) - 1;  // x of slot 0
+  const int y0 = yb * TY;
+  const int z0 = zc * a.rows;
+  const int z1 = min(z0 + a.rows, (int)g.S[2]);
+  const int SX = (int)g.S[0], SY = (int)g.S[1], SZ = (int)g.S[2];
+  const int j0 = warp, j1 = warp + NW;           // tile rows of the two halves
+  const int yr0 = y0 - 1 + j0, yr1 = y0 - 1 + j1;
+  const int xs = xw + lane;
+  const bool out_x = (lane >= 1) & (lane <= W - 2) & (xs < SX);
+  const bool in_x = (xs >= -1) & (xs <= SX);
+  const bool xface = (xs < g.pad) | (xs >= SX - g.pad);
+  const bool in0 = in_x & (yr0 <= SY), in1 = in_x & (yr1 <= SY);
+  const bool ok0 = out_x & (yr0 <= SY), ok1 = out_x & (yr1 <= SY);
+  const bool st0 = out_x & (j0 >= 1) & (yr0 < SY);                // stores: rows 1..TY
+  const bool st1 = out_x & (j1 <= TY) & (yr1 < SY);
+  const bool yface0 = (yr0 < g.pad) | (yr0 >= SY - g.pad);
+  const bool yface1 = (yr1 < g.pad) | (yr1 >= SY - g.pad);
+  Coef<float> kc;
+  if (!step_coef(a, kc)) return;
+  const bool ws = a.cf.dev != nullptr;
+  const float gam = (float)a.cf.gamma;
+  float wmax = 0.0f;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < SM::NS; ++s) mbar_init(&bar[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int sh = (int)(g.xo + xw) % SM::AL;
+  const int tx = (int)(g.xo + xw) - sh, ty = (int)(g.off[1] + y0 - 1);
+  const int nplanes = z1 - (z0 - 1) + 1;  // planes z0-1 .. z1
+  auto issue = [&](int kz) {
+    if (kz >= nplanes) return;
+    const int s = kz % SM::NS;
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * 4u);
+    tma_load_4d(stage + s * SM::STAGE, &tmap, &bar[s], tx, 0, ty, (int)(g.off[2] + z0 - 1 + kz));
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < SM::NS; ++s) issue(s);
+  }
+
+  pk zus[C], zfz[C], zph[C];  // z-march state: U** and F_z of the previous plane, last z-face
+  int bad = 0, nan = 0;
+  const pk gm1(a.gm1);
+  const pk qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]), nqy(kc.nq2[1]), qz(kc.q[2]), nqz(kc.nq2[2]);
+  const int64_t plane = g.rstride * g.P[1], cs = g.cstride;
+  float* dst0 = a.out + g.row(yr0, z0 - 1) * g.rstride + (g.xo + xs);
+  float* dst1 = a.out + g.row(yr1, z0 - 1) * g.rstride + (g.xo + xs);
+  // y-face rows: below row j (face j-1 | j) and above (face j | j+1), clamped into range
+  const int fb0 = max(j0 - 1, 0), fa1 = min(j1, R - 2);
+
+  for (int kz = 0; kz < nplanes; ++kz) {
+    const int z = z0 - 1 + kz;
+    const int s = kz % SM::NS;
+    mbar_wait(&bar[s], (kz / SM::NS) & 1);
+    // ---------------- X: rows j0 and j1
+    pk U[C], F[C], S_[C], G[C];
+    {
+      const float* r0 = stage + s * SM::STAGE + j0 * C * SM::WB + sh + lane;
+      const float* r1 = stage + s * SM::STAGE + j1 * C * SM::WB + sh + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) U[c] = pk(r0[c * SM::WB], r1[c * SM::WB]);
+    }
+    {
+      const PkDom b = phys_flux<D, 0>(U, F, gm1);
+      bad |= (in0 ? b.a : 0) | (in1 ? b.b : 0);
+    }
+    {
+      pk Un[C], Fn[C], Pnx[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Un[c] = shfl_down1(U[c]);
+        Fn[c] = shfl_down1(F[c]);
+      }
+      force_face<D, 0>(U, F, Un, Fn, Pnx, qx, nqx, gm1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) S_[c] = U[c] - (Pnx[c] - shfl_up1(Pnx[c]));
+    }
+    {
+      const PkDom b = phys_flux<D, 1>(S_, G, gm1);
+      bad |= (ok0 ? b.a : 0) | (ok1 ? b.b : 0);
+    }
+    {
+      float* x0 = xy + j0 * 2 * C * W + lane;
+      float* x1 = xy + j1 * 2 * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        x0[c * W] = S_[c].x;
+        x0[(C + c) * W] = G[c].x;
+        x1[c * W] = S_[c].y;
+        x1[(C + c) * W] = G[c].y;
+      }
+    }
+    __syncthreads();  // (A): stage s consumed, (U*, F_y) published
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      issue(kz + SM::NS);
+    }
+    // ---------------- Y: faces (j0-1 | j0) and (j1-1 | j1)
+    pk Py[C];
+    {
+      const float* p0 = xy + fb0 * 2 * C * W + lane;
+      const float* p1 = xy + (j1 - 1) * 2 * C * W + lane;
+      pk Sp[C], Gp[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Sp[c] = pk(p0[c * W], p1[c * W]);
+        Gp[c] = pk(p0[(C + c) * W], p1[(C + c) * W]);
+      }
+      force_face<D, 1>(Sp, Gp, S_, G, Py, qy, nqy, gm1);
+      float* f0 = fyb + fb0 * C * W + lane;
+      float* f1 = fyb + (j1 - 1) * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (j0 >= 1) f0[c * W] = Py[c].x;
+        f1[c * W] = Py[c].y;
+      }
+    }
+    __syncthreads();  // (B): y-faces published
+    // ---------------- Y update + Z march (row halves with outputs)
+    {
+      const float* u0 = fyb + j0 * C * W + lane;   // face (j0 | j0+1); j0 <= R-2 always
+      const float* u1 = fyb + fa1 * C * W + lane;  // face (j1 | j1+1)
+      pk Us[C], Gz[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) Us[c] = S_[c] - (pk(u0[c * W], u1[c * W]) - Py[c]);
+      {
+        const PkDom b = phys_flux<D, 2>(Us, Gz, gm1);
+        bad |= (st0 ? b.a : 0) | (st1 ? b.b : 0);
+      }
+      if (kz >= 1) {
+        pk Pz[C];
+        force_face<D, 2>(zus, zfz, Us, Gz, Pz, qz, nqz, gm1);
+        if (kz >= 2) {
+          // update and store plane z-1
+          pk o[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) o[c] = zus[c] - (Pz[c] - zph[c]);
+          dst0 += plane;
+          dst1 += plane;
+          const bool zf = (z - 1 < g.pad) | (z - 1 >= SZ - g.pad);
+          if (st0) {
+            float v[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) v[c] = o[c].x;
+            nan = max(nan, max(naninf(v[0]), naninf(v[C - 1])));
+            if (ws) wmax = fmaxf(wmax, wavespeed<D>(v, a.gm1, gam));
+#pragma unroll
+            for (int c = 0; c < C; ++c) dst0[c * cs] = v[c];
+            if (xface | yface0 | zf) {
+              if (g.img_fast)
+                images_single<D>(g, a.out, xs, yr0, z - 1, v);
+              else
+                images3_nl<D, 0, float>(&a, xs, yr0, z - 1, v[0], v[1], v[2], v[3], v[4]);
+            }
+          }
+          if (st1) {
+            float v[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) v[c] = o[c].y;
+            nan = max(nan, max(naninf(v[0]), naninf(v[C - 1])));
+            if (ws) wmax = fmaxf(wmax, wavespeed<D>(v, a.gm1, gam));
+#pragma unroll
+            for (int c = 0; c < C; ++c) dst1[c * cs] = v[c];
+            if (xface | yface1 | zf) {
+              if (g.img_fast)
+                images_single<D>(g, a.out, xs, yr1, z - 1, v);
+              else
+                images3_nl<D, 0, float>(&a, xs, yr1, z - 1, v[0], v[1], v[2], v[3], v[4]);
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) zph[c] = Pz[c];
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        zus[c] = Us[c];
+        zfz[c] = Gz[c];
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad < 0 || nan >= kExpMask<float>) && lane == 0) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -322,12 +548,51 @@ struct Cfg3 {
   static constexpr int W = 32 * V;
 };
 
-// tile rows of a 3-D launch (variants 50: 30 rows, 51: 22 rows; default 14)
-static int ty3(int variant) { return variant == 50 ? 30 : (variant == 51 ? 22 : 14); }
+// fp32 SoA runs the row-paired packed kernel k_step3d_rp unless a scalar variant
+// is asked for (20: k_step3d V = 1, 21: V = 2, 50-52: scalar tile shapes)
+// (default: 8 warps / 14 output rows, two CTAs per SM -- 1270 us at 384^3 vs
+// 1375 us for variant 70, 16 warps / 30 rows, one CTA per SM)
+static bool use_rp(const Geom& g, int variant) {
+  return g.elem == 4 && g.layout == 0 && (variant == 0 || variant == 70);
+}
+static int rp_warps(int variant) { return variant == 70 ? 16 : 8; }
+
+// tile rows of a 3-D launch (variants 50: 30 rows, 51: 22 rows; default 14;
+// fp32 SoA packed: 2 NW rows incl. the y-halo)
+static int ty3(const Geom& g, int variant) {
+  if (use_rp(g, variant)) return 2 * rp_warps(variant) - 2;
+  return variant == 50 ? 30 : (variant == 51 ? 22 : 14);
+}
 
 // x-window width of a 3-D launch (variant 21: fp32 with V = 2)
 static int win3(const Geom& g, int variant) {
   return (g.elem == 4 && variant == 21) ? 64 : 32;
+}
+
+// (-0.0f, -0.0f) into c_pk_negzero on the current device, once (packed.cuh)
+static void pk_set_negzero() {
+  static int done[kMaxDevices] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  if (done[dev]) return;
+  static const unsigned long long nz = 0x8000000080000000ull;
+  if (cudaMemcpyToSymbol(c_pk_negzero, &nz, sizeof(nz)) == cudaSuccess) done[dev] = 1;
+}
+
+template <int NW, int MB>
+static int launch3_rp(const KArgs<float>& a, const void* tmap, cudaStream_t s) {
+  constexpr int W = 32, TY = 2 * NW - 2;
+  const Geom& g = a.g;
+  const int nwin = (int)((g.S[0] + (W - 2) - 1) / (W - 2));
+  const int nyb = (int)((g.S[1] + TY - 1) / TY);
+  const int nzc = (int)((g.S[2] + a.rows - 1) / a.rows);
+  const size_t sm = SmemRP<NW>::bytes();
+  pk_set_negzero();
+  static int cache[kMaxDevices] = {0};
+  resident_ctas(k_step3d_rp<NW, MB>, 32 * NW, sm, cache);  // sets the smem attribute
+  k_step3d_rp<NW, MB><<<nwin * nyb * nzc, 32 * NW, sm, s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb);
+  return 0;
 }
 
 int make_tmap(const Geom& g, const void* buf, void* map_out, int box_w, int box_rows) {
@@ -367,9 +632,13 @@ static int launch3(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
 template <typename T>
 int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   if (a.g.layout == 1) return launch3<T, 1, 14, 1, 1>(a, tmap, s);  // AoS (configs[4])
-  // V = 2 (two cells per lane) only for fp32 -- must match win3() / the TMA box
-  if constexpr (sizeof(T) == 4)
+  if constexpr (sizeof(T) == 4) {
+    // packed row pairs (default) -- must match use_rp() / the TMA box
+    if (use_rp(a.g, a.variant))
+      return a.variant == 70 ? launch3_rp<16, 1>(a, tmap, s) : launch3_rp<8, 2>(a, tmap, s);
+    // V = 2 (two cells per lane) only for fp32 -- must match win3() / the TMA box
     if (a.variant == 21) return launch3<T, 2, 14>(a, tmap, s);
+  }
   switch (a.variant) {
     case 50: return launch3<T, 1, 30>(a, tmap, s);
     case 51: return launch3<T, 1, 22>(a, tmap, s);
@@ -399,7 +668,7 @@ int make_tmap_aos(const Geom& g, const void* buf, void* map_out, int box_cells, 
 int make_tmap3d(const Geom& g, const void* buf, void* map_out, int variant) {
   if (g.layout == 1) return make_tmap_aos(g, buf, map_out, 32 + 16 / g.elem, 14 + 2);
   return make_tmap(g, buf, map_out, win3(g, variant) + 16 / g.elem,  // + Smem3::AL
-                   ty3(variant) + 2);
+                   ty3(g, variant) + 2);
 }
 template int launch_step3d<float>(const KArgs<float>&, const void*, cudaStream_t);
 template int launch_step3d<double>(const KArgs<double>&, const void*, cudaStream_t);

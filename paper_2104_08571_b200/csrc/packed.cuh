@@ -1,0 +1,88 @@
+// packed.cuh -- two fp32 lanes of the scheme per instruction (sm_100a FFMA2 /
+// FADD2 / FMUL2, PTX add|sub|mul|fma.rn.f32x2).
+//
+// `pk` holds one component of two cells (a register pair).  The scheme's
+// templates in scheme.cuh (phys_flux, force_face) run unchanged on it, so a
+// packed kernel performs, per lane, exactly the IEEE operations of the scalar
+// fp32 kernels -- results are bitwise identical.
+// Measured on the B200 (tools/dp_microbench.cu): FFMA2 delivers the same lane
+// rate as FFMA (126 lane-FMA/clk/SM) from half the issue slots, which is what
+// the issue-bound fp32 3-D step needs.
+//
+// One ptxas caveat: it contracts mul.rn.f32x2 + add/sub.rn.f32x2 into FFMA2
+// even under --fmad=false (and folds fma(a, b, -0) back to a multiply first),
+// which would break bit-identity with the scalar kernels.  Products are
+// therefore issued as fma(a, b, z) with z = -0.0 read from constant memory that
+// the host sets at run time (pk_set_negzero): the compiler cannot see the
+// value, so the multiply stays a stand-alone FFMA2 and fma(a, b, -0) == a*b
+// exactly (including the sign of zero).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "scheme.cuh"
+
+namespace rpl {
+
+// (-0.0f, -0.0f) -- written by the host (pk_set_negzero) before any packed launch
+static __constant__ unsigned long long c_pk_negzero;
+
+struct __align__(8) pk {
+  float x, y;
+  __device__ __forceinline__ pk() {}
+  __device__ __forceinline__ pk(float a, float b) : x(a), y(b) {}
+  template <typename S>
+  __device__ __forceinline__ explicit pk(S s) : x((float)s), y((float)s) {}
+};
+
+__device__ __forceinline__ unsigned long long pbits(pk a) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ pk punpack(unsigned long long r) {
+  pk a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+
+__device__ __forceinline__ pk operator+(pk a, pk b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pbits(a)), "l"(pbits(b)));
+  return punpack(r);
+}
+__device__ __forceinline__ pk operator-(pk a, pk b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pbits(a)), "l"(pbits(b)));
+  return punpack(r);
+}
+__device__ __forceinline__ pk operator*(pk a, pk b) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pbits(a)), "l"(pbits(b)), "l"(c_pk_negzero));
+  return punpack(r);
+}
+__device__ __forceinline__ pk operator-(pk a) { return pk(-a.x, -a.y); }
+__device__ __forceinline__ pk fma(pk a, pk b, pk c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pbits(a)), "l"(pbits(b)), "l"(pbits(c)));
+  return punpack(r);
+}
+// 1/x per lane: the scalar MUFU + Newton sequence of scheme.cuh
+__device__ __forceinline__ pk rcp(pk a) { return pk(rcp(a.x), rcp(a.y)); }
+
+// domain word per lane (scheme.cuh dom_word)
+struct PkDom {
+  int a, b;
+};
+__device__ __forceinline__ PkDom dom_word(pk rho, pk p) {
+  return PkDom{dom_word(rho.x, p.x), dom_word(rho.y, p.y)};
+}
+
+__device__ __forceinline__ pk shfl_down1(pk v) {
+  return pk(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+}
+__device__ __forceinline__ pk shfl_up1(pk v) {
+  return pk(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+}
+
+}  // namespace rpl

@@ -423,10 +423,13 @@ def test_full_size_sampled_flux_difference_fd8k():
                     <= 1e-4 * scale, gy
 
 
-@pytest.mark.parametrize("variant,dtype", [("21", "f32"), ("21", "f64"), ("51", "f64"),
+@pytest.mark.parametrize("variant,dtype", [("0", "f32"), ("20", "f32"), ("21", "f32"),
+                                           ("70", "f32"), ("21", "f64"), ("51", "f64"),
                                            ("51", "f32")])
 def test_3d_kernel_variants_bitwise(variant, dtype, monkeypatch):
-    """3-D fused variants (RPL_VARIANT: 21 = two cells per lane for fp32, the default
+    """3-D fused variants (RPL_VARIANT: 0 = default, for fp32 SoA the packed
+    row-pair kernel (FFMA2, 8 warps / 14 rows); 70 = packed, 16 warps / 30 rows;
+    20 = scalar one cell per lane; 21 = two cells per lane for fp32, the default
     for fp64; 51 = 22-row tiles) give bitwise the split kernel's result (ragged
     windows, tiles and z-chunks)."""
     n = (70, 33, 20)

@@ -20,6 +20,32 @@ __global__ void fma_tp(T* out, int iters, T a, T b) {
   if (s == (T)-1) out[threadIdx.x] = s;
 }
 
+// packed FP32 (sm_100a FFMA2): two lanes' worth of FMA per issued instruction
+template <int ILP>
+__global__ void fma2_tp(float* out, int iters, float a, float b) {
+  unsigned long long acc[ILP];
+  const float2 av = make_float2(a, a), bv = make_float2(b, b);
+  const unsigned long long A = *reinterpret_cast<const unsigned long long*>(&av);
+  const unsigned long long B = *reinterpret_cast<const unsigned long long*>(&bv);
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) {
+    const float2 v = make_float2((float)(threadIdx.x + i), (float)i);
+    acc[i] = *reinterpret_cast<const unsigned long long*>(&v);
+  }
+  for (int k = 0; k < iters; ++k) {
+#pragma unroll
+    for (int i = 0; i < ILP; ++i)
+      asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(acc[i]) : "l"(A), "l"(B));
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) {
+    const float2 v = *reinterpret_cast<const float2*>(&acc[i]);
+    s += v.x + v.y;
+  }
+  if (s == -1.0f) out[threadIdx.x] = s;
+}
+
 __global__ void rcp_tp(double* out, int iters) {
   double x[8];
 #pragma unroll
@@ -78,6 +104,14 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     if (rep) printf("fp32 FMA: %.1f TFLOP/s  (%.2f lane-FMA/clk/SM)\n", flops / ms / 1e9,
                     flops / 2 / (ms * 1e-3) / sms / 1.965e9);
+    cudaEventRecord(e0);
+    fma2_tp<8><<<blocks, threads>>>(f, iters, 1.0000001f, 1e-9f);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep) printf("fp32x2 FFMA2: %.1f TFLOP/s  (%.2f lane-FMA/clk/SM, %.2f FFMA2 warp-instr/clk/SM)\n",
+                    2 * flops / ms / 1e9, flops / (ms * 1e-3) / sms / 1.965e9,
+                    flops / (ms * 1e-3) / sms / 1.965e9 / 64);
     cudaEventRecord(e0);
     rcp_tp<<<blocks, threads>>>(d, iters / 4);
     cudaEventRecord(e1);
