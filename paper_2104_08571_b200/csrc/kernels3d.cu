@@ -569,16 +569,6 @@ static int win3(const Geom& g, int variant) {
   return (g.elem == 4 && variant == 21) ? 64 : 32;
 }
 
-// (-0.0f, -0.0f) into c_pk_negzero on the current device, once (packed.cuh)
-static void pk_set_negzero() {
-  static int done[kMaxDevices] = {0};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
-  if (done[dev]) return;
-  static const unsigned long long nz = 0x8000000080000000ull;
-  if (cudaMemcpyToSymbol(c_pk_negzero, &nz, sizeof(nz)) == cudaSuccess) done[dev] = 1;
-}
-
 template <int NW, int MB>
 static int launch3_rp(const KArgs<float>& a, const void* tmap, cudaStream_t s) {
   constexpr int W = 32, TY = 2 * NW - 2;

@@ -20,12 +20,24 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "launch.cuh"
 #include "scheme.cuh"
 
 namespace rpl {
 
-// (-0.0f, -0.0f) -- written by the host (pk_set_negzero) before any packed launch
+// (-0.0f, -0.0f) -- written by the host (pk_set_negzero) before any packed launch;
+// one copy per translation unit (static), each set by its own launchers
 static __constant__ unsigned long long c_pk_negzero;
+
+// Host: write c_pk_negzero of this translation unit on the current device, once.
+static inline void pk_set_negzero() {
+  static int done[kMaxDevices] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  if (done[dev]) return;
+  static const unsigned long long nz = 0x8000000080000000ull;
+  if (cudaMemcpyToSymbol(c_pk_negzero, &nz, sizeof(nz)) == cudaSuccess) done[dev] = 1;
+}
 
 struct __align__(8) pk {
   float x, y;
@@ -62,6 +74,7 @@ __device__ __forceinline__ pk operator*(pk a, pk b) {
   return punpack(r);
 }
 __device__ __forceinline__ pk operator-(pk a) { return pk(-a.x, -a.y); }
+using ::fma;  // keep the scalar overloads visible next to the packed one
 __device__ __forceinline__ pk fma(pk a, pk b, pk c) {
   unsigned long long r;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pbits(a)), "l"(pbits(b)), "l"(pbits(c)));

@@ -1129,6 +1129,7 @@ static rpl_status fluxdiff_t(rpl_domain* d, double dt) {
   }
   a.gm1 = (T)(d->cfg.gamma - 1.0);
   a.flag = d->d_flag;
+  a.variant = d->variant;
   // fused config, 2-D SoA: tiled kernel (each face once); otherwise the plain one
   const bool tiled = d->cfg.kernel == RPL_KERNEL_FUSED && g.D == 2 && g.layout == 0;
   if (tiled && !d->fd_tmaps) {

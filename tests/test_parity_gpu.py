@@ -354,6 +354,24 @@ def test_2d_kernel_variants_bitwise(variant, parts, monkeypatch):
     assert np.array_equal(run_gpu(U0, dt, 7, dx=dx, parts=parts), ref)
 
 
+@pytest.mark.parametrize("variant", ["0", "20", "73"])
+def test_flux_difference_fp32_variants_bitwise(variant, monkeypatch):
+    """f2 fp32 tiled kernels (RPL_VARIANT: 0 = packed row pairs, FFMA2, 8 warps x 4
+    CTAs; 73 = the same, 3 CTAs; 20 = scalar one row per warp) == per-cell kernel."""
+    n = (1000, 333)
+    dx = [1.0 / n[0]] * 2
+    U0 = W.shock_bubble(n, dx=dx).astype(np.float32)
+    out = []
+    for kernel in ("split", "fused"):
+        if kernel == "fused":
+            monkeypatch.setenv("RPL_VARIANT", variant)
+        with R.Domain(n, pad=1, dtype="f32", dx=dx, kernel=kernel) as dom:
+            dom.set_state(U0)
+            dom.flux_difference(2e-4)
+            out.append(dom.get_flux_difference())
+    assert np.array_equal(out[0], out[1])
+
+
 def _sample_boxes(n, size, count, seed):
     """Patch origins: the corners plus seeded interior positions."""
     rng = np.random.default_rng(seed)
