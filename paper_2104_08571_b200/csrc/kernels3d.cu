@@ -301,7 +301,7 @@ struct SmemRP {
   static constexpr size_t bytes() { return (size_t)(NS * STAGE + XY + FY) * 4 + 64; }
 };
 
-template <int NW, int MB>
+template <int NW, int MB, int L>
 __global__ void __launch_bounds__(32 * NW, MB)
     k_step3d_rp(const __grid_constant__ KArgs<float> a, const __grid_constant__ CUtensorMap tmap,
                 int nwin, int nyb) {
@@ -355,7 +355,8 @@ __global__ void __launch_bounds__(32 * NW, MB)
     if (kz >= nplanes) return;
     const int s = kz % SM::NS;
     mbar_arrive_expect_tx(&bar[s], SM::STAGE * 4u);
-    tma_load_4d(stage + s * SM::STAGE, &tmap, &bar[s], tx, 0, ty, (int)(g.off[2] + z0 - 1 + kz));
+    tma_load_4d(stage + s * SM::STAGE, &tmap, &bar[s], L == 0 ? tx : tx * C, 0, ty,
+                (int)(g.off[2] + z0 - 1 + kz));
   };
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -367,8 +368,8 @@ __global__ void __launch_bounds__(32 * NW, MB)
   const pk gm1(a.gm1);
   const pk qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]), nqy(kc.nq2[1]), qz(kc.q[2]), nqz(kc.nq2[2]);
   const int64_t plane = g.rstride * g.P[1], cs = g.cstride;
-  float* dst0 = a.out + g.row(yr0, z0 - 1) * g.rstride + (g.xo + xs);
-  float* dst1 = a.out + g.row(yr1, z0 - 1) * g.rstride + (g.xo + xs);
+  float* dst0 = a.out + g.row(yr0, z0 - 1) * g.rstride + (g.xo + xs) * g.xstride;
+  float* dst1 = a.out + g.row(yr1, z0 - 1) * g.rstride + (g.xo + xs) * g.xstride;
   // y-face rows: below row j (face j-1 | j) and above (face j | j+1), clamped into range
   const int fb0 = max(j0 - 1, 0), fa1 = min(j1, R - 2);
 
@@ -379,10 +380,13 @@ __global__ void __launch_bounds__(32 * NW, MB)
     // ---------------- X: rows j0 and j1
     pk U[C], F[C], S_[C], G[C];
     {
-      const float* r0 = stage + s * SM::STAGE + j0 * C * SM::WB + sh + lane;
-      const float* r1 = stage + s * SM::STAGE + j1 * C * SM::WB + sh + lane;
+      // stage row layout: SoA box [C][WB] (x fastest), AoS box [WB][C] (component fastest)
+      constexpr int cst = L == 0 ? SM::WB : 1;
+      const int xo = L == 0 ? sh + lane : (sh + lane) * C;
+      const float* r0 = stage + s * SM::STAGE + j0 * C * SM::WB + xo;
+      const float* r1 = stage + s * SM::STAGE + j1 * C * SM::WB + xo;
 #pragma unroll
-      for (int c = 0; c < C; ++c) U[c] = pk(r0[c * SM::WB], r1[c * SM::WB]);
+      for (int c = 0; c < C; ++c) U[c] = pk(r0[c * cst], r1[c * cst]);
     }
     {
       const PkDom b = phys_flux<D, 0>(U, F, gm1);
@@ -474,7 +478,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
               if (g.img_fast)
                 images_single<D>(g, a.out, xs, yr0, z - 1, v);
               else
-                images3_nl<D, 0, float>(&a, xs, yr0, z - 1, v[0], v[1], v[2], v[3], v[4]);
+                images3_nl<D, L, float>(&a, xs, yr0, z - 1, v[0], v[1], v[2], v[3], v[4]);
             }
           }
           if (st1) {
@@ -489,7 +493,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
               if (g.img_fast)
                 images_single<D>(g, a.out, xs, yr1, z - 1, v);
               else
-                images3_nl<D, 0, float>(&a, xs, yr1, z - 1, v[0], v[1], v[2], v[3], v[4]);
+                images3_nl<D, L, float>(&a, xs, yr1, z - 1, v[0], v[1], v[2], v[3], v[4]);
             }
           }
         }
@@ -548,12 +552,13 @@ struct Cfg3 {
   static constexpr int W = 32 * V;
 };
 
-// fp32 SoA runs the row-paired packed kernel k_step3d_rp unless a scalar variant
-// is asked for (20: k_step3d V = 1, 21: V = 2, 50-52: scalar tile shapes)
+// fp32 runs the row-paired packed kernel k_step3d_rp unless a scalar variant is
+// asked for (20: k_step3d V = 1, 21: V = 2, 50-52: scalar tile shapes); AoS
+// (configs[4] layout comparison) only in the 8-warp form
 // (default: 8 warps / 14 output rows, two CTAs per SM -- 1270 us at 384^3 vs
 // 1375 us for variant 70, 16 warps / 30 rows, one CTA per SM)
 static bool use_rp(const Geom& g, int variant) {
-  return g.elem == 4 && g.layout == 0 && (variant == 0 || variant == 70);
+  return g.elem == 4 && (variant == 0 || (variant == 70 && g.layout == 0));
 }
 static int rp_warps(int variant) { return variant == 70 ? 16 : 8; }
 
@@ -569,7 +574,7 @@ static int win3(const Geom& g, int variant) {
   return (g.elem == 4 && variant == 21) ? 64 : 32;
 }
 
-template <int NW, int MB>
+template <int NW, int MB, int L>
 static int launch3_rp(const KArgs<float>& a, const void* tmap, cudaStream_t s) {
   constexpr int W = 32, TY = 2 * NW - 2;
   const Geom& g = a.g;
@@ -579,8 +584,8 @@ static int launch3_rp(const KArgs<float>& a, const void* tmap, cudaStream_t s) {
   const size_t sm = SmemRP<NW>::bytes();
   pk_set_negzero();
   static int cache[kMaxDevices] = {0};
-  resident_ctas(k_step3d_rp<NW, MB>, 32 * NW, sm, cache);  // sets the smem attribute
-  k_step3d_rp<NW, MB><<<nwin * nyb * nzc, 32 * NW, sm, s>>>(
+  resident_ctas(k_step3d_rp<NW, MB, L>, 32 * NW, sm, cache);  // sets the smem attribute
+  k_step3d_rp<NW, MB, L><<<nwin * nyb * nzc, 32 * NW, sm, s>>>(
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb);
   return 0;
 }
@@ -621,11 +626,15 @@ static int launch3(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
 
 template <typename T>
 int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
-  if (a.g.layout == 1) return launch3<T, 1, 14, 1, 1>(a, tmap, s);  // AoS (configs[4])
   if constexpr (sizeof(T) == 4) {
     // packed row pairs (default) -- must match use_rp() / the TMA box
-    if (use_rp(a.g, a.variant))
-      return a.variant == 70 ? launch3_rp<16, 1>(a, tmap, s) : launch3_rp<8, 2>(a, tmap, s);
+    if (use_rp(a.g, a.variant)) {
+      if (a.g.layout == 1) return launch3_rp<8, 2, 1>(a, tmap, s);  // AoS (configs[4])
+      return a.variant == 70 ? launch3_rp<16, 1, 0>(a, tmap, s) : launch3_rp<8, 2, 0>(a, tmap, s);
+    }
+  }
+  if (a.g.layout == 1) return launch3<T, 1, 14, 1, 1>(a, tmap, s);  // AoS (configs[4])
+  if constexpr (sizeof(T) == 4) {
     // V = 2 (two cells per lane) only for fp32 -- must match win3() / the TMA box
     if (a.variant == 21) return launch3<T, 2, 14>(a, tmap, s);
   }
