@@ -510,13 +510,15 @@ def main():
         launches_per_step = 1
     peak, peak_src = measured_peak_gbs()
     alg_bytes = 2 * C * elem * local_cells  # per step-kernel launch (one partition per rank)
-    kname = {"fused": {1: "k_sweep", 2: "k_step2d_pt", 3: "k_step3d"}[D], "split": "k_sweep"}[args.kernel]
+    kname = {"fused": {1: "k_sweep", 2: "k_step2d_pt",
+                       3: "k_step3d_rp" if wl["dtype"] == "f32" else "k_step3d"}[D],
+             "split": "k_sweep"}[args.kernel]
     if wl.get("order", 1) == 2:
-        kname = {2: "k_step2d_o2", 3: "k_step2d_o2<3> (x-y) + k_sweep2 (z)"}.get(D, "k_sweep2") \
+        kname = {2: "k_step2d_o2", 3: "k_step2d_o2<3> (x-y) + k_zmarch2 (z)"}.get(D, "k_sweep2") \
             if (args.kernel == "fused" and args.layout == "soa") else "k_sweep2"
     if op == "fluxdiff":
-        kname = "k_fluxdiff_pt" if (args.kernel == "fused" and D == 2 and args.layout == "soa") \
-            else "k_fluxdiff"
+        kname = ("k_fluxdiff_rp" if wl["dtype"] == "f32" else "k_fluxdiff_pt") \
+            if (args.kernel == "fused" and D == 2 and args.layout == "soa") else "k_fluxdiff"
     per_launch_ms = kern_ms / max(kern_launches, 1)
     launches_per_step_kernel = max(1, kern_launches // max(5, min(args.steps, 20)))
     if args.kernel == "split" or D != 2:
@@ -524,8 +526,12 @@ def main():
     else:
         alg_bytes_launch = alg_bytes
     achieved = alg_bytes_launch / (per_launch_ms / 1e3) / 1e9
-    traffic = ncu_traffic(f"{args.workload}_{wl['dtype']}_{args.layout}") \
-        if args.workload == "l256" else ncu_traffic(f"{args.workload}_{args.kernel}")
+    if args.workload == "l256":
+        traffic = ncu_traffic(f"{args.workload}_{wl['dtype']}_{args.layout}")
+    elif op == "fluxdiff" and wl["dtype"] == "f64":
+        traffic = ncu_traffic(f"{args.workload}_f64")
+    else:
+        traffic = ncu_traffic(f"{args.workload}_{args.kernel}")
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
             "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json copy bandwidth, burst)",
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,

@@ -35,6 +35,12 @@ def relerr(g, o):
     return max(errs)
 
 
+def bits_equal(a, b):
+    """Bit-pattern equality (np.array_equal treats -0.0 == +0.0; this does not)."""
+    it = {4: np.uint32, 8: np.uint64}[a.dtype.itemsize]
+    return a.dtype == b.dtype and np.array_equal(a.view(it), b.view(it))
+
+
 def run_gpu(U0, dt, nsteps, dtype="f64", **kw):
     n = tuple(reversed(U0.shape[:-1]))
     with R.Domain(n, dtype=dtype, **kw) as dom:
@@ -261,7 +267,7 @@ def test_fused3d_equals_split_bitwise(dtype, n, rows):
               bc_hi=["clamp", "periodic", "reflective"])
     a = run_gpu(U0, dt, 12, kernel="fused", rows_per_chunk=rows, **kw)
     b = run_gpu(U0, dt, 12, kernel="split", **kw)
-    assert np.array_equal(a, b)
+    assert bits_equal(a, b)
 
 
 def test_fused3d_partitioned_ghosts_sound():
@@ -337,7 +343,7 @@ def test_flux_difference_tiled_equals_plain_bitwise(dtype, n, pad, parts):
             dom.set_state(U0)
             dom.flux_difference(2e-4)
             out.append(dom.get_flux_difference())
-    assert np.array_equal(out[0], out[1])
+    assert bits_equal(out[0], out[1])
 
 
 @pytest.mark.parametrize("variant", ["31", "34", "37", "44", "46"])
@@ -369,7 +375,7 @@ def test_flux_difference_fp32_variants_bitwise(variant, monkeypatch):
             dom.set_state(U0)
             dom.flux_difference(2e-4)
             out.append(dom.get_flux_difference())
-    assert np.array_equal(out[0], out[1])
+    assert bits_equal(out[0], out[1])
 
 
 def _sample_boxes(n, size, count, seed):
@@ -458,7 +464,7 @@ def test_3d_kernel_variants_bitwise(variant, dtype, monkeypatch):
     dt = 0.4 * dx[0] / 5.8
     ref = run_gpu(U0, dt, 5, dtype=dtype, kernel="split", dx=dx, rows_per_chunk=7)
     monkeypatch.setenv("RPL_VARIANT", variant)
-    assert np.array_equal(run_gpu(U0, dt, 5, dtype=dtype, dx=dx, rows_per_chunk=7), ref)
+    assert bits_equal(run_gpu(U0, dt, 5, dtype=dtype, dx=dx, rows_per_chunk=7), ref)
 
 
 def test_configs1_full_field_100_steps():
