@@ -496,6 +496,25 @@ def test_minimum_sizes(n, bc, kernel):
     assert relerr(Ug, Uo) <= 1e-10
 
 
+@pytest.mark.parametrize("n", [(2, 2, 2), (3, 2, 5), (2, 17, 3), (31, 15, 2), (33, 16, 17)])
+@pytest.mark.parametrize("bc", ["clamp", "periodic", "reflective"])
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+def test_minimum_sizes_fp32_packed(n, bc, layout):
+    """The packed fp32 3-D kernel (two tile rows per lane) at degenerate and
+    tile-edge extents (one row pair half empty, x just past one window, y just
+    past one 14-row tile): bit pattern of the split kernel, and the fp32 oracle."""
+    D = 3
+    dx = [1.0 / 8] * D
+    U0 = W.random_state(n, seed=19).astype(np.float32)
+    dt = 0.2 * dx[0] / 3.0
+    kw = dict(bc_lo=[bc] * D, bc_hi=[bc] * D)
+    Ug = run_gpu(U0, dt, 4, dtype="f32", dx=dx, layout=layout, **kw)
+    Us = run_gpu(U0, dt, 4, dtype="f32", dx=dx, kernel="split", **kw)
+    assert bits_equal(Ug, Us)
+    Uo = run_oracle(U0, dt, 4, dx, **kw)
+    assert relerr(Ug, Uo) <= 1e-4
+
+
 def test_zero_steps_and_repeated_calls_compose():
     """advance(dt, 0) is a no-op; advance(dt, 3) == three advance(dt, 1) calls (bitwise)."""
     n = (70, 40)
