@@ -443,11 +443,14 @@ def main():
         kern = dom.profile_read() if profile else (0.0, 0)
         if profile:
             dom.profile(0)
-        return sum(a.elapsed_time(b) for a, b in ev) / 1e3, kern
+        per_step = [a.elapsed_time(b) for a, b in ev]  # ms
+        timed_loop.last_steps = per_step
+        return sum(per_step) / 1e3, kern
 
     wall0 = time.perf_counter()
     with Clocks(dev) as clk:
         t_total, _ = timed_loop(args.steps, profile=False)   # the headline timing
+    step_list = list(timed_loop.last_steps)
     wall = time.perf_counter() - wall0
     # the dominant kernel's own launch time for the roofline (separate, profiled pass)
     n_prof = max(5, min(args.steps, 20))
@@ -460,6 +463,10 @@ def main():
                           device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_total = float(tt.item())
+        ts = torch.tensor(step_list, dtype=torch.float64,
+                          device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        step_list = ts.cpu().tolist()
     dom.synchronize()  # surfaces any domain error of the timed steps
 
     # ---- e2e through the public API with host buffers (pinned), copies timed
@@ -559,7 +566,11 @@ def main():
     line = {"metric": "Gcell/s (flux difference)" if op == "fluxdiff" else "Gcell-updates/s",
             "value": value, "unit": "Gcell/s" if op == "fluxdiff" else "Gcell-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True,
+            "ms_per_step": t_total / args.steps * 1e3,
+            "step_ms": {"min": min(step_list), "median": statistics.median(step_list),
+                        "max": max(step_list), "n": len(step_list),
+                        "how": "per-step CUDA events (max over ranks per step)"},
+            "higher_is_better": True,
             "scaling": wl["scaling"], "vs_baseline": vs, "dtype": wl["dtype"],
             "data": "synthetic",
             "config": {"workload": wl["label"], "global_cells": gn, "parts": parts,
