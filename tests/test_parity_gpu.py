@@ -212,6 +212,28 @@ def test_domain_error_is_reported():
             dom.synchronize()
 
 
+@pytest.mark.parametrize("dtype,layout", [("f32", "soa"), ("f32", "aos"), ("f64", "soa")])
+@pytest.mark.parametrize("where", ["interior", "corner", "last_row"])
+def test_domain_error_is_reported_3d(dtype, layout, where):
+    """3-D fused kernels (packed fp32 incl.): one cell with negative pressure -- in the
+    interior, at a domain corner, or in the last row half of a packed row pair --
+    raises at the next synchronising call; a clean state of the same run does not."""
+    n = (40, 30, 20)
+    U0 = W.uniform(n, rho=1.0, vel=[0.1, 0.0, -0.2], p=1.0).astype(
+        np.float32 if dtype == "f32" else np.float64)
+    with R.Domain(n, dtype=dtype, layout=layout) as dom:
+        dom.set_state(U0)
+        dom.advance(1e-3, 2)
+        dom.synchronize()  # clean
+    z, y, x = {"interior": (10, 13, 21), "corner": (0, 0, 0), "last_row": (7, 29, 39)}[where]
+    U0[z, y, x, 4] = -1.0
+    with R.Domain(n, dtype=dtype, layout=layout) as dom:
+        dom.set_state(U0)
+        dom.advance(1e-3, 1)
+        with pytest.raises(R.DomainError):
+            dom.synchronize()
+
+
 def test_uniform_state_bitwise_full_size():
     """BASELINE configs[1] size and launch configuration: uniform state is a fixed point."""
     n = (1024, 1024)
