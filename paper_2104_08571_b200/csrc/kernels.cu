@@ -179,7 +179,7 @@ __device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map, 
       : "memory");
 }
 
-template <typename T, int V, int NW>
+template <typename T, int V, int NW, int NS = 2>
 struct SmemPT {
   static constexpr int W = 32 * V, C = 4;
   // TMA boxes must start 16-byte aligned in x: load AL extra elements from the
@@ -189,19 +189,20 @@ struct SmemPT {
   static constexpr int STAGE = NW * C * WB;
   static constexpr int XY = NW * 2 * C * W;
   static constexpr int FY = (NW - 1) * C * W;
-  static constexpr size_t bytes() { return (size_t)(2 * STAGE + XY + FY) * sizeof(T) + 64; }
+  static constexpr size_t bytes() { return (size_t)(NS * STAGE + XY + FY) * sizeof(T) + 64; }
 };
 
-template <typename T, int V, int NW, int MB>
+// NS: depth of the TMA ring (tiles in flight ahead of the compute)
+template <typename T, int V, int NW, int MB, int NS = 2>
 __global__ void __launch_bounds__(32 * NW, MB)
     k_step2d_pt(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
                 int nwin, int ntiles) {
   constexpr int D = 2, C = 4, W = 32 * V;
-  using SM = SmemPT<T, V, NW>;
+  using SM = SmemPT<T, V, NW, NS>;
   using VT = typename VecV<T, V>::type;
   extern __shared__ __align__(1024) unsigned char smem[];
   T* stage = reinterpret_cast<T*>(smem);
-  T* xy = stage + 2 * SM::STAGE;
+  T* xy = stage + NS * SM::STAGE;
   T* fy = xy + SM::XY;
   uint64_t* bar = reinterpret_cast<uint64_t*>(fy + SM::FY);
   const Geom& g = a.g;
@@ -215,15 +216,15 @@ __global__ void __launch_bounds__(32 * NW, MB)
   T wmax = T(0);
   const T gm1 = a.gm1, qx = kc.q[0], nqx = kc.nq2[0], qy = kc.q[1], nqy = kc.nq2[1];
   if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) mbar_init(&bar[k], 1);
     fence_barrier_init();
   }
   __syncthreads();
   auto issue = [&](int i) {
     const int tile = blockIdx.x + i * G;
     if (tile >= ntiles) return;
-    const int s = i & 1;
+    const int s = i % NS;
     const int w = tile % nwin, yb = tile / nwin;
     mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
     const int x0 = (int)g.xo + w * (W - 2) - 1;
@@ -231,13 +232,13 @@ __global__ void __launch_bounds__(32 * NW, MB)
                  (int)g.off[1] + yb * (NW - 2) - 1, 0);
   };
   if (threadIdx.x == 0) {
-    issue(0);
-    issue(1);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) issue(k);
   }
   int bad = 0, nan = 0;
   // loop-invariant addresses (hoisted by hand: the asm barriers/TMA calls in the
   // loop would otherwise make the compiler recompute them every tile)
-  const unsigned bar_a0 = smem_u32(&bar[0]), bar_a1 = smem_u32(&bar[1]);
+  const unsigned bar_a0 = smem_u32(&bar[0]);
   const T* const st_lane = stage + warp * C * SM::WB + V * lane;
   T* const xr_lane = xy + warp * 2 * C * W + V * lane;
   T* const out_lane = a.out + (int64_t)g.xo + V * lane;
@@ -253,8 +254,8 @@ __global__ void __launch_bounds__(32 * NW, MB)
     const int yr = yb * (NW - 2) - 1 + warp;
     const bool row_in = yr <= SY;
     const bool row_out = (warp >= 1) & (warp <= NW - 2) & (yr < SY);
-    const int s = i & 1;
-    mbar_wait_u32(s ? bar_a1 : bar_a0, (i >> 1) & 1);
+    const int s = NS == 2 ? (i & 1) : i % NS;
+    mbar_wait_u32(bar_a0 + 8 * s, (i / NS) & 1);
     // ---- X
     T U[V][C], F[V][C], S_[V][C], G_[V][C];
     {
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
     __syncthreads();  // (A) stage s consumed; (U*, F_y) published
     if (threadIdx.x == 0) {
       fence_proxy_async();
-      issue(i + 2);
+      issue(i + NS);
     }
     // ---- Y face between rows warp-1 and warp
     T Py[V][C];
@@ -431,19 +432,19 @@ __global__ void __launch_bounds__(32 * NW, MB)
   if (ws) publish_max(a, wmax);
 }
 
-template <typename T, int V, int NW, int MB = (V == 1 ? 2 : 1)>
+template <typename T, int V, int NW, int MB = (V == 1 ? 2 : 1), int NS = 2>
 static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   constexpr int W = 32 * V;
-  using SM = SmemPT<T, V, NW>;
+  using SM = SmemPT<T, V, NW, NS>;
   const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((a.g.S[1] + (NW - 2) - 1) / (NW - 2));
   const int ntiles = nwin * nyb;
   static int cache[kMaxDevices] = {0};
-  const int per_sm = resident_ctas(k_step2d_pt<T, V, NW, MB>, 32 * NW, SM::bytes(), cache);
+  const int per_sm = resident_ctas(k_step2d_pt<T, V, NW, MB, NS>, 32 * NW, SM::bytes(), cache);
   const int nsm = sm_count();
   int grid = per_sm * nsm;
   if (grid > ntiles) grid = ntiles;
-  k_step2d_pt<T, V, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
+  k_step2d_pt<T, V, NW, MB, NS><<<grid, 32 * NW, SM::bytes(), s>>>(
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
 }
 
@@ -788,7 +789,7 @@ int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
     case 33: v = 2; nw = 16; break;
     case 36: v = 2; nw = 8; break;
     case 38: nw = 10; break;
-    case 44: nw = 24; break;
+    case 44: case 45: nw = 24; break;
     case 46: nw = 14; break;
     case 47: nw = 20; break;
     default: nw = 12; break;  // 0, 37, 39
@@ -961,6 +962,9 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 44: return launch_pt2d<T, 1, 24, 1>(a, tmap, s);
     case 46: return launch_pt2d<T, 1, 14, 2>(a, tmap, s);
     case 47: return launch_pt2d<T, 1, 20, 1>(a, tmap, s);
+    case 48: return launch_pt2d<T, 1, 12, 2, 3>(a, tmap, s);  // 3-stage TMA ring
+    case 49: return launch_pt2d<T, 1, 12, 2, 4>(a, tmap, s);  // 4-stage TMA ring
+    case 45: return launch_pt2d<T, 1, 24, 1, 3>(a, tmap, s);
     default: return launch_pt2d<T, 1, 12, 2>(a, tmap, s);  // 0 / 37: the default
   }
 }
