@@ -945,6 +945,16 @@ int auto_rows_3d(const Geom& g) {
   return (int)rows;
 }
 
+// Default 2-D order-1 tile shape.  12-row tiles, 2 CTAs/SM (variant 0/37) at
+// small partitions, where their finer granularity shortens the last wave (1024^2:
+// 28.9 us vs 29.9 us for 24-row tiles); 24-row tiles, 1 CTA/SM, 3-stage ring
+// (variant 45: 10 of 12 vs 22 of 24 rows are outputs) once a partition has >= 32
+// such tiles per SM (6400x4000: 450 us vs 475 us; profiles/r1/tile_shape_2d.txt).
+int auto_variant_2d(const Geom& g) {
+  const int64_t tiles24 = ((g.S[0] + 29) / 30) * ((g.S[1] + 21) / 22);
+  return tiles24 >= 32LL * sm_count() ? 45 : 0;
+}
+
 template <typename T>
 void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   if (a.order == 2) return launch_step2d_o2<T>(a, tmap, s);

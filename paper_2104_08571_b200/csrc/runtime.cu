@@ -418,6 +418,8 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
   CU(cudaMalloc(&d->d_cfl, sizeof(CflDev)));
   CU(cudaMallocHost(&d->h_cfl, sizeof(CflDev)));
   if (const char* v = getenv("RPL_VARIANT")) d->variant = atoi(v);
+  // 2-D order 1: large partitions take the 24-row / 3-stage tile (no wave tail to lose)
+  if (d->variant == 0 && g.D == 2 && g.layout == 0 && c->order == 1) d->variant = auto_variant_2d(g);
   if (g.D == 3) {  // SoA and AoS
     d->tmaps_ok = true;
     for (int p : d->local)
