@@ -617,6 +617,9 @@ static rpl_status xfer(rpl_domain* d, void* host, bool to_dev, int which = -1) {
 static rpl_status check_flag(rpl_domain* d) {
   CU(cudaMemcpyAsync(d->h_flag, d->d_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, d->stream));
   CU(cudaStreamSynchronize(d->stream));
+  if (*d->h_flag & 2u)
+    return fail(RPL_E_CUDA, "P2P transport: a peer rank did not reach the step epoch within "
+                            "RPL_P2P_TIMEOUT_S (default 120 s)");
   if (*d->h_flag)
     return fail(RPL_E_DOMAIN, "numerical-domain error: rho<=0, p<=0 or non-finite state (S:588)");
   return RPL_OK;
@@ -690,8 +693,18 @@ static rpl_status exchange_t(rpl_domain* d, int b) {
 // the peers' slot set `set` and, after the wait, reduces its own set into *smax
 // (exact: max).  Sets rotate with the step (device CFL): a rank is at most one
 // epoch ahead of any peer, so a set is never rewritten before it was read.
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Bounded wait: a peer that never reaches this epoch (crashed or hung process)
+// sets bit 1 of the sticky flag after timeout_ns instead of spinning forever;
+// the next synchronising call reports it (RPL_E_CUDA).
 __global__ void k_p2p_sync(unsigned long long* const* ctl, int me, int nranks,
-                           unsigned long long epoch, unsigned long long* smax, int set, int mode) {
+                           unsigned long long epoch, unsigned long long* smax, int set, int mode,
+                           unsigned* flag, unsigned long long timeout_ns) {
   const int r = threadIdx.x;
   unsigned long long* mine = ctl[me];
   const int so = kMaxParts * (1 + set);
@@ -705,9 +718,16 @@ __global__ void k_p2p_sync(unsigned long long* const* ctl, int me, int nranks,
     __threadfence_system();
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer + me), "l"(epoch) : "memory");
     unsigned long long got = 0;
+    const unsigned long long t0 = globaltimer_ns();
     do {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(got) : "l"(mine + r) : "memory");
-      if (got < epoch) __nanosleep(64);
+      if (got < epoch) {
+        __nanosleep(64);
+        if (globaltimer_ns() - t0 > timeout_ns) {
+          atomicOr(flag, 2u);
+          break;
+        }
+      }
     } while (got < epoch);
   }
   __syncwarp();
@@ -728,8 +748,13 @@ static rpl_status p2p_sync(rpl_domain* d, int mode, unsigned long long* smax = n
                            int set = 0) {
   if (!d->p2p_attached) return fail(RPL_E_INVALID_ARG, "P2P transport: call rpl_p2p_attach first");
   ++d->epoch;
+  static const unsigned long long timeout_ns = [] {
+    const char* e = getenv("RPL_P2P_TIMEOUT_S");
+    const double sec = e ? atof(e) : 120.0;
+    return (unsigned long long)((sec > 0 ? sec : 120.0) * 1e9);
+  }();
   k_p2p_sync<<<1, 32, 0, d->stream>>>(d->d_peer_ctl, d->cfg.rank, d->cfg.nranks, d->epoch,
-                                      smax ? smax : d->d_smax, set, mode);
+                                      smax ? smax : d->d_smax, set, mode, d->d_flag, timeout_ns);
   CU(cudaGetLastError());
   return RPL_OK;
 }

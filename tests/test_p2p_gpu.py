@@ -117,6 +117,58 @@ def test_p2p_eight_ranks_bitwise_equal_single_rank(n, parts, kw):
 
 
 
+def _stall_rank(rank, port, q):
+    """Rank 1 attaches and then never steps; rank 0 steps and must get an error from
+    the bounded P2P wait (RPL_P2P_TIMEOUT_S) instead of hanging."""
+    import sys
+    import time
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ["RPL_P2P_TIMEOUT_S"] = "2"
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_08571_b200 as R
+    import workloads as W
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        torch.cuda.set_device(0)
+        n = (64, 64)
+        dom = R.Domain(n, parts=(1, 2), nranks=2, rank=rank, transport="p2p")
+        blobs = [None] * 2
+        dist.all_gather_object(blobs, dom.p2p_export())
+        dom.p2p_attach(blobs)
+        if rank == 0:
+            dom.set_state(W.random_state(n, box=(dom.lo, dom.hi)))  # no peer sync here
+            t0 = time.time()
+            err = None
+            try:
+                dom.advance(1e-4, 1)
+                dom.synchronize()
+            except R.RplError as e:
+                err = str(e)
+            q.put((err, time.time() - t0))
+        dist.barrier()  # rank 1 idles here until rank 0 is done
+        dom.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_stalled_peer_times_out():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_stall_rank, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    err, dt = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+    assert err is not None and "P2P" in err, err
+    assert dt < 60
+
+
 def _check(n, parts, kw, t_end):
     world = int(np.prod(parts))
     steps = 6
