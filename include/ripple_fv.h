@@ -78,7 +78,10 @@ typedef enum { RPL_KERNEL_FUSED = 0, RPL_KERNEL_SPLIT = 1 } rpl_kernel;
  *        buffer over NVLink peer memory (CUDA IPC mappings), then a one-warp
  *        flag kernel orders the step against the neighbours (system-scope
  *        release/acquire); no pack, no copy, no NCCL.  Needs rpl_p2p_export /
- *        rpl_p2p_attach after rpl_create and a library-owned arena. */
+ *        rpl_p2p_attach after rpl_create and a library-owned arena.  The flag
+ *        wait is bounded: a peer that does not arrive within RPL_P2P_TIMEOUT_S
+ *        seconds (environment, default 120) makes the next synchronising call
+ *        return RPL_E_CUDA instead of hanging. */
 typedef enum { RPL_TRANSPORT_NCCL = 0, RPL_TRANSPORT_P2P = 1 } rpl_transport;
 
 typedef struct {
