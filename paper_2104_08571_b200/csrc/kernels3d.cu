@@ -511,6 +511,225 @@ __global__ void __launch_bounds__(32 * NW, MB)
   if (ws) publish_max(a, wmax);
 }
 
+
+// ------------------------------------------------------------------------
+// fp32, adjacent row pairs (the fp32 default): warp w owns tile rows 2w and 2w+1, so the
+// y-face between them is computed in registers, packed with the face below row
+// 2w (one force_face for both); only row 2w+1's (U*, F_y) and the face below row
+// 2w go through shared memory (half the hand-off traffic of k_step3d_rp).  Same
+// per-cell and per-face operations: bitwise equal to k_step3d / k_sweep.
+// ------------------------------------------------------------------------
+template <int NW>
+struct SmemRA {
+  static constexpr int W = 32, R = 2 * NW, C = 5, NS = 2;
+  static constexpr int AL = 4;
+  static constexpr int WB = W + AL;
+  static constexpr int STAGE = R * C * WB;
+  static constexpr int XY = NW * 2 * C * W;  // (U*, F_y) of row 2w+1, per warp
+  static constexpr int FY = NW * C * W;      // face below row 2w, per warp
+  static constexpr size_t bytes() { return (size_t)(NS * STAGE + XY + FY) * 4 + 64; }
+};
+
+template <int NW, int MB, int L>
+__global__ void __launch_bounds__(32 * NW, MB)
+    k_step3d_ra(const __grid_constant__ KArgs<float> a, const __grid_constant__ CUtensorMap tmap,
+                int nwin, int nyb) {
+  constexpr int D = 3, C = 5, W = 32, R = 2 * NW, TY = R - 2;
+  using SM = SmemRA<NW>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  float* stage = reinterpret_cast<float*>(smem);
+  float* xy = stage + SM::NS * SM::STAGE;
+  float* fyb = xy + SM::XY;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + SM::FY);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int t = blockIdx.x;
+  const int win = t % nwin;
+  t /= nwin;
+  const int yb = t % nyb;
+  const int zc = t / nyb;
+  const int xw = win * (W - 2) - 1;
+  const int y0 = yb * TY;
+  const int z0 = zc * a.rows;
+  const int z1 = min(z0 + a.rows, (int)g.S[2]);
+  const int SX = (int)g.S[0], SY = (int)g.S[1], SZ = (int)g.S[2];
+  const int j0 = 2 * warp, j1 = 2 * warp + 1;
+  const int yr0 = y0 - 1 + j0, yr1 = y0 - 1 + j1;
+  const int xs = xw + lane;
+  const bool out_x = (lane >= 1) & (lane <= W - 2) & (xs < SX);
+  const bool in_x = (xs >= -1) & (xs <= SX);
+  const bool xface = (xs < g.pad) | (xs >= SX - g.pad);
+  const bool in0 = in_x & (yr0 <= SY), in1 = in_x & (yr1 <= SY);
+  const bool ok0 = out_x & (yr0 <= SY), ok1 = out_x & (yr1 <= SY);
+  const bool st0 = out_x & (j0 >= 1) & (yr0 < SY);
+  const bool st1 = out_x & (j1 <= TY) & (yr1 < SY);
+  const bool yface0 = (yr0 < g.pad) | (yr0 >= SY - g.pad);
+  const bool yface1 = (yr1 < g.pad) | (yr1 >= SY - g.pad);
+  Coef<float> kc;
+  if (!step_coef(a, kc)) return;
+  const bool ws = a.cf.dev != nullptr;
+  const float gam = (float)a.cf.gamma;
+  float wmax = 0.0f;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < SM::NS; ++s) mbar_init(&bar[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int sh = (int)(g.xo + xw) % SM::AL;
+  const int tx = (int)(g.xo + xw) - sh, ty = (int)(g.off[1] + y0 - 1);
+  const int nplanes = z1 - (z0 - 1) + 1;
+  auto issue = [&](int kz) {
+    if (kz >= nplanes) return;
+    const int s = kz % SM::NS;
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * 4u);
+    tma_load_4d(stage + s * SM::STAGE, &tmap, &bar[s], L == 0 ? tx : tx * C, 0, ty,
+                (int)(g.off[2] + z0 - 1 + kz));
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < SM::NS; ++s) issue(s);
+  }
+
+  pk zus[C], zfz[C], zph[C];
+  int bad = 0, nan = 0;
+  const pk gm1(a.gm1);
+  const pk qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]), nqy(kc.nq2[1]), qz(kc.q[2]), nqz(kc.nq2[2]);
+  const int64_t plane = g.rstride * g.P[1], cs = g.cstride;
+  float* dst0 = a.out + g.row(yr0, z0 - 1) * g.rstride + (g.xo + xs) * g.xstride;
+  float* dst1 = a.out + g.row(yr1, z0 - 1) * g.rstride + (g.xo + xs) * g.xstride;
+  // row 2w-1 lives in warp w-1's slot (warp 0: its own slot, value unused)
+  const int wdn = max(warp - 1, 0), wup = min(warp + 1, NW - 1);
+
+  for (int kz = 0; kz < nplanes; ++kz) {
+    const int z = z0 - 1 + kz;
+    const int s = kz % SM::NS;
+    mbar_wait(&bar[s], (kz / SM::NS) & 1);
+    pk U[C], F[C], S_[C], G[C];
+    {
+      constexpr int cst = L == 0 ? SM::WB : 1;
+      const int xo = L == 0 ? sh + lane : (sh + lane) * C;
+      const float* r0 = stage + s * SM::STAGE + j0 * C * SM::WB + xo;
+      const float* r1 = stage + s * SM::STAGE + j1 * C * SM::WB + xo;
+#pragma unroll
+      for (int c = 0; c < C; ++c) U[c] = pk(r0[c * cst], r1[c * cst]);
+    }
+    {
+      const PkDom b = phys_flux<D, 0>(U, F, gm1);
+      bad |= (in0 ? b.a : 0) | (in1 ? b.b : 0);
+    }
+    {
+      pk Un[C], Fn[C], Pnx[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Un[c] = shfl_down1(U[c]);
+        Fn[c] = shfl_down1(F[c]);
+      }
+      force_face<D, 0>(U, F, Un, Fn, Pnx, qx, nqx, gm1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) S_[c] = U[c] - (Pnx[c] - shfl_up1(Pnx[c]));
+    }
+    {
+      const PkDom b = phys_flux<D, 1>(S_, G, gm1);
+      bad |= (ok0 ? b.a : 0) | (ok1 ? b.b : 0);
+    }
+    {
+      float* x1 = xy + warp * 2 * C * W + lane;  // row 2w+1 for warp w+1
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        x1[c * W] = S_[c].y;
+        x1[(C + c) * W] = G[c].y;
+      }
+    }
+    __syncthreads();  // (A)
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      issue(kz + SM::NS);
+    }
+    // ---------------- Y: faces (2w-1 | 2w) and (2w | 2w+1) in one packed evaluation
+    pk Py[C];
+    {
+      const float* pd = xy + wdn * 2 * C * W + lane;
+      pk SL[C], GL[C], SR[C], GR[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        SL[c] = pk(pd[c * W], S_[c].x);
+        GL[c] = pk(pd[(C + c) * W], G[c].x);
+        SR[c] = pk(S_[c].x, S_[c].y);
+        GR[c] = pk(G[c].x, G[c].y);
+      }
+      force_face<D, 1>(SL, GL, SR, GR, Py, qy, nqy, gm1);
+      float* f0 = fyb + warp * C * W + lane;  // face below row 2w, for warp w-1
+#pragma unroll
+      for (int c = 0; c < C; ++c) f0[c * W] = Py[c].x;
+    }
+    __syncthreads();  // (B)
+    {
+      const float* fu = fyb + wup * C * W + lane;  // face below row 2w+2 (warp w+1)
+      pk Us[C], Gz[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        Us[c] = S_[c] - (pk(Py[c].y, fu[c * W]) - pk(Py[c].x, Py[c].y));
+      {
+        const PkDom b = phys_flux<D, 2>(Us, Gz, gm1);
+        bad |= (st0 ? b.a : 0) | (st1 ? b.b : 0);
+      }
+      if (kz >= 1) {
+        pk Pz[C];
+        force_face<D, 2>(zus, zfz, Us, Gz, Pz, qz, nqz, gm1);
+        if (kz >= 2) {
+          pk o[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) o[c] = zus[c] - (Pz[c] - zph[c]);
+          dst0 += plane;
+          dst1 += plane;
+          const bool zf = (z - 1 < g.pad) | (z - 1 >= SZ - g.pad);
+          if (st0) {
+            float v[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) v[c] = o[c].x;
+            nan = max(nan, max(naninf(v[0]), naninf(v[C - 1])));
+            if (ws) wmax = fmaxf(wmax, wavespeed<D>(v, a.gm1, gam));
+#pragma unroll
+            for (int c = 0; c < C; ++c) dst0[c * cs] = v[c];
+            if (xface | yface0 | zf) {
+              if (g.img_fast)
+                images_single<D>(g, a.out, xs, yr0, z - 1, v);
+              else
+                images3_nl<D, L, float>(&a, xs, yr0, z - 1, v[0], v[1], v[2], v[3], v[4]);
+            }
+          }
+          if (st1) {
+            float v[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) v[c] = o[c].y;
+            nan = max(nan, max(naninf(v[0]), naninf(v[C - 1])));
+            if (ws) wmax = fmaxf(wmax, wavespeed<D>(v, a.gm1, gam));
+#pragma unroll
+            for (int c = 0; c < C; ++c) dst1[c * cs] = v[c];
+            if (xface | yface1 | zf) {
+              if (g.img_fast)
+                images_single<D>(g, a.out, xs, yr1, z - 1, v);
+              else
+                images3_nl<D, L, float>(&a, xs, yr1, z - 1, v[0], v[1], v[2], v[3], v[4]);
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) zph[c] = Pz[c];
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        zus[c] = Us[c];
+        zfz[c] = Gz[c];
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad < 0 || nan >= kExpMask<float>) && lane == 0) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -555,10 +774,11 @@ struct Cfg3 {
 // fp32 runs the row-paired packed kernel k_step3d_rp unless a scalar variant is
 // asked for (20: k_step3d V = 1, 21: V = 2, 50-52: scalar tile shapes); AoS
 // (configs[4] layout comparison) only in the 8-warp form
-// (default: 8 warps / 14 output rows, two CTAs per SM -- 1270 us at 384^3 vs
-// 1375 us for variant 70, 16 warps / 30 rows, one CTA per SM)
+// (default k_step3d_ra, 8 warps / 14 output rows, two CTAs per SM: 384^3 1047 us;
+// variant 78 k_step3d_rp 1111 us; variant 70, 16 warps / 30 rows, one CTA per SM,
+// slower still)
 static bool use_rp(const Geom& g, int variant) {
-  return g.elem == 4 && (variant == 0 || (variant == 70 && g.layout == 0));
+  return g.elem == 4 && (variant == 0 || variant == 78 || (variant == 70 && g.layout == 0));
 }
 static int rp_warps(int variant) { return variant == 70 ? 16 : 8; }
 
@@ -572,6 +792,22 @@ static int ty3(const Geom& g, int variant) {
 // x-window width of a 3-D launch (variant 21: fp32 with V = 2)
 static int win3(const Geom& g, int variant) {
   return (g.elem == 4 && variant == 21) ? 64 : 32;
+}
+
+template <int NW, int MB, int L>
+static int launch3_ra(const KArgs<float>& a, const void* tmap, cudaStream_t s) {
+  constexpr int W = 32, TY = 2 * NW - 2;
+  const Geom& g = a.g;
+  const int nwin = (int)((g.S[0] + (W - 2) - 1) / (W - 2));
+  const int nyb = (int)((g.S[1] + TY - 1) / TY);
+  const int nzc = (int)((g.S[2] + a.rows - 1) / a.rows);
+  const size_t sm = SmemRA<NW>::bytes();
+  pk_set_negzero();
+  static int cache[kMaxDevices] = {0};
+  resident_ctas(k_step3d_ra<NW, MB, L>, 32 * NW, sm, cache);
+  k_step3d_ra<NW, MB, L><<<nwin * nyb * nzc, 32 * NW, sm, s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb);
+  return 0;
 }
 
 template <int NW, int MB, int L>
@@ -629,8 +865,12 @@ int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   if constexpr (sizeof(T) == 4) {
     // packed row pairs (default) -- must match use_rp() / the TMA box
     if (use_rp(a.g, a.variant)) {
-      if (a.g.layout == 1) return launch3_rp<8, 2, 1>(a, tmap, s);  // AoS (configs[4])
-      return a.variant == 70 ? launch3_rp<16, 1, 0>(a, tmap, s) : launch3_rp<8, 2, 0>(a, tmap, s);
+      // default: adjacent row pairs (k_step3d_ra); 78: rows w, w+8 (k_step3d_rp); 70: the
+      // same with 16 warps / 30 rows
+      if (a.variant == 70) return launch3_rp<16, 1, 0>(a, tmap, s);
+      if (a.variant == 78)
+        return a.g.layout == 1 ? launch3_rp<8, 2, 1>(a, tmap, s) : launch3_rp<8, 2, 0>(a, tmap, s);
+      return a.g.layout == 1 ? launch3_ra<8, 2, 1>(a, tmap, s) : launch3_ra<8, 2, 0>(a, tmap, s);
     }
   }
   if (a.g.layout == 1) return launch3<T, 1, 14, 1, 1>(a, tmap, s);  // AoS (configs[4])
