@@ -524,7 +524,7 @@ def main():
         kname = {2: "k_step2d_o2", 3: "k_step2d_o2<3> (x-y) + k_zmarch2 (z)"}.get(D, "k_sweep2") \
             if (args.kernel == "fused" and args.layout == "soa") else "k_sweep2"
     if op == "fluxdiff":
-        kname = ("k_fluxdiff_rp" if wl["dtype"] == "f32" else "k_fluxdiff_pt") \
+        kname = ("k_fluxdiff_ra" if wl["dtype"] == "f32" else "k_fluxdiff_pt") \
             if (args.kernel == "fused" and D == 2 and args.layout == "soa") else "k_fluxdiff"
     per_launch_ms = kern_ms / max(kern_launches, 1)
     launches_per_step_kernel = max(1, kern_launches // max(5, min(args.steps, 20)))

@@ -1388,15 +1388,170 @@ static void launch_fd_rp(const KArgs<float>& a, const void* tmap, cudaStream_t s
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
 }
 
+
+// fp32 default: adjacent row pairs -- warp w owns rows 2w and 2w+1, the y-face
+// between them is computed in registers together with the face below row 2w
+// (one packed force_face); only row 2w+1's (U, F_y) and that lower face go
+// through shared memory.  Same operations per face and cell: bitwise equal.
+template <int NW, int MB>
+__global__ void __launch_bounds__(32 * NW, MB)
+    k_fluxdiff_ra(const __grid_constant__ KArgs<float> a, const __grid_constant__ CUtensorMap tmap,
+                  int nwin, int ntiles) {
+  constexpr int D = 2, C = 4, W = 32, R = 2 * NW;
+  using SM = SmemFD<float, R>;  // stage geometry of the 2 NW-row box
+  extern __shared__ __align__(1024) unsigned char smem[];
+  float* stage = reinterpret_cast<float*>(smem);
+  float* uf = stage + 2 * SM::STAGE;
+  float* fyb = uf + NW * 2 * C * W;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + NW * C * W);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = 2 * warp, j1 = 2 * warp + 1;
+  const int wdn = max(warp - 1, 0), wup = min(warp + 1, NW - 1);
+  const int SX = (int)g.S[0], SY = (int)g.S[1];
+  const int G = gridDim.x;
+  const pk gm1(a.gm1);
+  const pk ilx(0.25f / a.q[0]), ily(0.25f / a.q[1]);
+  const pk qx(a.q[0]), nqx(a.nq2[0]), qy(a.q[1]), nqy(a.nq2[1]);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int i) {
+    const int tile = blockIdx.x + i * G;
+    if (tile >= ntiles) return;
+    const int s = i & 1;
+    const int w = tile % nwin, yb = tile / nwin;
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * 4u);
+    const int x0 = (int)g.xo + w * (W - 2) - 1;
+    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
+                 (int)g.off[1] + yb * (R - 2) - 1, 0);
+  };
+  if (threadIdx.x == 0) {
+    issue(0);
+    issue(1);
+  }
+  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
+  int win = (int)blockIdx.x % nwin, yb = (int)blockIdx.x / nwin;
+  const int nyb = ntiles / nwin;
+  for (int i = 0;; ++i) {
+    if (yb >= nyb) break;
+    const int xw = win * (W - 2) - 1;
+    const int yr0 = yb * (R - 2) - 1 + j0, yr1 = yr0 + 1;
+    const int s = i & 1;
+    mbar_wait(&bar[s], (i >> 1) & 1);
+    pk U[C], Fx[C], Fy[C], Rx[C];
+    {
+      const int sh = ((int)g.xo + xw) % SM::AL;
+      const float* s0 = stage + s * SM::STAGE + j0 * C * SM::WB + sh + lane;
+      const float* s1 = s0 + C * SM::WB;
+#pragma unroll
+      for (int c = 0; c < C; ++c) U[c] = pk(s0[c * SM::WB], s1[c * SM::WB]);
+    }
+    phys_flux<D, 0>(U, Fx, gm1);
+    phys_flux<D, 1>(U, Fy, gm1);
+    {
+      pk Un[C], Fn[C], Pnx[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Un[c] = shfl_down1(U[c]);
+        Fn[c] = shfl_down1(Fx[c]);
+      }
+      force_face<D, 0>(U, Fx, Un, Fn, Pnx, qx, nqx, gm1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) Rx[c] = fma(Pnx[c] - shfl_up1(Pnx[c]), ilx, pk(0.0f));
+    }
+    {
+      float* w1 = uf + warp * 2 * C * W + lane;  // row 2w+1 for warp w+1
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        w1[c * W] = U[c].y;
+        w1[(C + c) * W] = Fy[c].y;
+      }
+    }
+    __syncthreads();  // (A)
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      issue(i + 2);
+    }
+    pk Py[C];
+    {
+      const float* pd = uf + wdn * 2 * C * W + lane;
+      pk UL[C], FL[C], UR[C], FR[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        UL[c] = pk(pd[c * W], U[c].x);
+        FL[c] = pk(pd[(C + c) * W], Fy[c].x);
+        UR[c] = pk(U[c].x, U[c].y);
+        FR[c] = pk(Fy[c].x, Fy[c].y);
+      }
+      force_face<D, 1>(UL, FL, UR, FR, Py, qy, nqy, gm1);
+      float* f0 = fyb + warp * C * W + lane;  // face below row 2w, for warp w-1
+#pragma unroll
+      for (int c = 0; c < C; ++c) f0[c * W] = Py[c].x;
+    }
+    __syncthreads();  // (B)
+    {
+      const bool xok = lane >= 1 && lane <= 30 && xw + lane < SX;
+      const bool ok0 = xok && j0 >= 1 && yr0 < SY;
+      const bool ok1 = xok && j1 <= R - 2 && yr1 < SY;
+      const float* fu = fyb + wup * C * W + lane;  // face below row 2w+2
+      pk o[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        o[c] = fma(pk(Py[c].y, fu[c * W]) - pk(Py[c].x, Py[c].y), ily, Rx[c]);
+      const int64_t cs = g.cstride;
+      if (ok0) {
+        float* dst = a.out + ((int64_t)((int)g.off[1] + yr0) * g.rstride + (int)g.xo + xw + lane);
+#pragma unroll
+        for (int c = 0; c < C; ++c) dst[c * cs] = o[c].x;
+      }
+      if (ok1) {
+        float* dst = a.out + ((int64_t)((int)g.off[1] + yr1) * g.rstride + (int)g.xo + xw + lane);
+#pragma unroll
+        for (int c = 0; c < C; ++c) dst[c * cs] = o[c].y;
+      }
+    }
+    win += Gr;
+    yb += Gq;
+    if (win >= nwin) {
+      win -= nwin;
+      ++yb;
+    }
+  }
+}
+
+template <int NW, int MB>
+static void launch_fd_ra(const KArgs<float>& a, const void* tmap, cudaStream_t s) {
+  constexpr int W = 32, R = 2 * NW, C = 4;
+  using SM = SmemFD<float, R>;
+  const size_t bytes = (size_t)(2 * SM::STAGE + NW * 3 * C * W) * 4 + 64;
+  const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
+  const int nyb = (int)((a.g.S[1] + (R - 2) - 1) / (R - 2));
+  const int ntiles = nwin * nyb;
+  pk_set_negzero();
+  static int cache[kMaxDevices] = {0};
+  const int per_sm = resident_ctas(k_fluxdiff_ra<NW, MB>, 32 * NW, bytes, cache);
+  const int nsm = sm_count();
+  int grid = per_sm * nsm;
+  if (grid > ntiles) grid = ntiles;
+  k_fluxdiff_ra<NW, MB><<<grid, 32 * NW, bytes, s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
+}
+
 int fd_tile_rows(int elem) { return 16; }
 
 template <typename T>
 void launch_fluxdiff_tiled(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   if constexpr (sizeof(T) == 4) {
-    // packed row pairs (8 warps, the same 16-row box) unless RPL_VARIANT=20 (scalar)
+    // packed row pairs (8 warps, the same 16-row box): adjacent rows (default), rows
+    // w, w+8 (78; 73: 3 CTAs/SM); RPL_VARIANT=20: scalar
     if (a.variant == 20) return launch_fd_pt<T, 16, 2>(a, tmap, s);
     if (a.variant == 73) return launch_fd_rp<8, 3>(a, tmap, s);
-    return launch_fd_rp<8, 4>(a, tmap, s);
+    if (a.variant == 78) return launch_fd_rp<8, 4>(a, tmap, s);
+    return launch_fd_ra<8, 4>(a, tmap, s);  // adjacent row pairs (default)
   }
   return launch_fd_pt<T, 16, 2>(a, tmap, s);
 }

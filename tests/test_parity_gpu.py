@@ -382,10 +382,11 @@ def test_2d_kernel_variants_bitwise(variant, parts, monkeypatch):
     assert np.array_equal(run_gpu(U0, dt, 7, dx=dx, parts=parts), ref)
 
 
-@pytest.mark.parametrize("variant", ["0", "20", "73"])
+@pytest.mark.parametrize("variant", ["0", "20", "73", "78"])
 def test_flux_difference_fp32_variants_bitwise(variant, monkeypatch):
-    """f2 fp32 tiled kernels (RPL_VARIANT: 0 = packed row pairs, FFMA2, 8 warps x 4
-    CTAs; 73 = the same, 3 CTAs; 20 = scalar one row per warp) == per-cell kernel."""
+    """f2 fp32 tiled kernels (RPL_VARIANT: 0 = packed adjacent row pairs, FFMA2, 8 warps
+    x 4 CTAs; 78 = packed rows w, w+8; 73 = the same, 3 CTAs; 20 = scalar one row per
+    warp) == per-cell kernel."""
     n = (1000, 333)
     dx = [1.0 / n[0]] * 2
     U0 = W.shock_bubble(n, dx=dx).astype(np.float32)
