@@ -576,3 +576,22 @@ def test_order2_periodic_conservation_and_symmetry():
 def test_order2_requires_pad2():
     with pytest.raises(ValueError):
         oracle.step(oracle.Grid((16,), pad=1, order=2), W.sod(16), 0.01, 1)
+
+
+def test_shock_bubble_robustness_oracle():
+    """the Mach-3.81 shock-bubble problem (reading S22) run for
+    1000 CFL steps (Listing 8's wavespeed -> max -> dt loop) stays physical: rho > 0,
+    p > 0 and finite everywhere, while the shock crosses the bubble (desk-scaled 128^2;
+    the GPU runs 512^2 in tests/test_cfl_gpu.py)."""
+    n = (128, 128)
+    dx = [1.0 / 128] * 2
+    U0 = W.shock_bubble(n, dx=dx)
+    U, steps = oracle.run_cfl(oracle.Grid(n, dx=dx), U0, 10.0, max_steps=1000)
+    assert steps == 1000
+    assert np.all(np.isfinite(U))
+    rho = U[..., 0]
+    p = 0.4 * (U[..., 3] - 0.5 * (U[..., 1] ** 2 + U[..., 2] ** 2) / rho)
+    assert rho.min() > 0 and p.min() > 0
+    # the shock has passed the bubble (centre x = 0.4): the post-shock density 4.46 of
+    # the initial state left of x = 0.1 now fills the domain's right half
+    assert rho[:, 96:].mean() > 2.0
