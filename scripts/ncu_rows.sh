@@ -15,7 +15,7 @@ cap o2_1024 k_step2d_o2 --workload o2_1024 --steps 3
 cap o2_s256_xy k_step2d_o2 --workload o2_s256 --steps 2
 cap o2_s256_z k_zmarch2 --workload o2_s256 --steps 2
 cap fd8k_f64 k_fluxdiff_pt --workload fd8k --dtype f64 --steps 3
-cap fd8k k_fluxdiff_rp --workload fd8k --steps 3
+cap fd8k k_fluxdiff_ra --workload fd8k --steps 3
 cap l256_f32_soa k_step3d --workload l256 --dtype f32 --steps 2
 cap l256_f32_aos k_step3d --workload l256 --dtype f32 --layout aos --steps 2
 cap l256_f64_soa k_step3d --workload l256 --dtype f64 --steps 2
