@@ -762,28 +762,20 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// tile geometry: V = 1 (32-slot windows) for both dtypes -- fp32 V = 2 (64
-// slots) is variant 21 (measured slower: 1.93 vs 1.35 ms at 384^3)
-template <typename T>
-struct Cfg3 {
-  static constexpr int V = 1;
-  static constexpr int TY = 14;
-  static constexpr int W = 32 * V;
-};
-
-// fp32 runs the row-paired packed kernel k_step3d_rp unless a scalar variant is
-// asked for (20: k_step3d V = 1, 21: V = 2, 50-52: scalar tile shapes); AoS
-// (configs[4] layout comparison) only in the 8-warp form
-// (default k_step3d_ra, 8 warps / 14 output rows, two CTAs per SM: 384^3 1047 us;
-// variant 78 k_step3d_rp 1111 us; variant 70, 16 warps / 30 rows, one CTA per SM,
-// slower still)
+// Tile geometry.  fp64: k_step3d with 32-slot windows (V = 1) and 14-row tiles.
+// fp32 runs a packed kernel unless a scalar variant is asked for (20: k_step3d
+// V = 1; 21: V = 2, 64-slot windows, measured slower: 1.93 vs 1.35 ms at 384^3;
+// 50-52: scalar tile shapes): by default k_step3d_ra (adjacent row pairs, 8 warps
+// / 14 output rows, two CTAs per SM: 384^3 1047 us); 78: k_step3d_rp (rows w,
+// w+8: 1111 us); 70: k_step3d_rp with 16 warps / 30 rows, one CTA per SM (slower
+// still, SoA only).  AoS (configs[4] layout comparison) runs the 8-warp forms.
 static bool use_rp(const Geom& g, int variant) {
   return g.elem == 4 && (variant == 0 || variant == 78 || (variant == 70 && g.layout == 0));
 }
 static int rp_warps(int variant) { return variant == 70 ? 16 : 8; }
 
 // tile rows of a 3-D launch (variants 50: 30 rows, 51: 22 rows; default 14;
-// fp32 SoA packed: 2 NW rows incl. the y-halo)
+// fp32 packed: 2 NW - 2 output rows, the box holds 2 NW rows incl. the y-halo)
 static int ty3(const Geom& g, int variant) {
   if (use_rp(g, variant)) return 2 * rp_warps(variant) - 2;
   return variant == 50 ? 30 : (variant == 51 ? 22 : 14);
