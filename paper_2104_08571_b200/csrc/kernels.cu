@@ -1378,7 +1378,7 @@ static void launch_fd_rp(const KArgs<float>& a, const void* tmap, cudaStream_t s
   const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((a.g.S[1] + (R - 2) - 1) / (R - 2));
   const int ntiles = nwin * nyb;
-  pk_set_negzero();
+  pk_set_negzero(s);
   static int cache[kMaxDevices] = {0};
   const int per_sm = resident_ctas(k_fluxdiff_rp<NW, MB>, 32 * NW, SM::bytes(), cache);
   const int nsm = sm_count();
@@ -1531,7 +1531,7 @@ static void launch_fd_ra(const KArgs<float>& a, const void* tmap, cudaStream_t s
   const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((a.g.S[1] + (R - 2) - 1) / (R - 2));
   const int ntiles = nwin * nyb;
-  pk_set_negzero();
+  pk_set_negzero(s);
   static int cache[kMaxDevices] = {0};
   const int per_sm = resident_ctas(k_fluxdiff_ra<NW, MB>, 32 * NW, bytes, cache);
   const int nsm = sm_count();

@@ -794,7 +794,7 @@ static int launch3_ra(const KArgs<float>& a, const void* tmap, cudaStream_t s) {
   const int nyb = (int)((g.S[1] + TY - 1) / TY);
   const int nzc = (int)((g.S[2] + a.rows - 1) / a.rows);
   const size_t sm = SmemRA<NW>::bytes();
-  pk_set_negzero();
+  pk_set_negzero(s);
   static int cache[kMaxDevices] = {0};
   resident_ctas(k_step3d_ra<NW, MB, L>, 32 * NW, sm, cache);
   k_step3d_ra<NW, MB, L><<<nwin * nyb * nzc, 32 * NW, sm, s>>>(
@@ -810,7 +810,7 @@ static int launch3_rp(const KArgs<float>& a, const void* tmap, cudaStream_t s) {
   const int nyb = (int)((g.S[1] + TY - 1) / TY);
   const int nzc = (int)((g.S[2] + a.rows - 1) / a.rows);
   const size_t sm = SmemRP<NW>::bytes();
-  pk_set_negzero();
+  pk_set_negzero(s);
   static int cache[kMaxDevices] = {0};
   resident_ctas(k_step3d_rp<NW, MB, L>, 32 * NW, sm, cache);  // sets the smem attribute
   k_step3d_rp<NW, MB, L><<<nwin * nyb * nzc, 32 * NW, sm, s>>>(

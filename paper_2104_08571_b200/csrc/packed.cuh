@@ -29,14 +29,20 @@ namespace rpl {
 // one copy per translation unit (static), each set by its own launchers
 static __constant__ unsigned long long c_pk_negzero;
 
-// Host: write c_pk_negzero of this translation unit on the current device, once.
-static inline void pk_set_negzero() {
+// Host: write c_pk_negzero of this translation unit on the current device, once,
+// ordered before the caller's launch on `stream` and completed before returning
+// (a pageable cudaMemcpyToSymbol may return before its DMA lands, and the
+// library's stream does not synchronise with the legacy stream).
+static inline void pk_set_negzero(cudaStream_t stream) {
   static int done[kMaxDevices] = {0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
   if (done[dev]) return;
   static const unsigned long long nz = 0x8000000080000000ull;
-  if (cudaMemcpyToSymbol(c_pk_negzero, &nz, sizeof(nz)) == cudaSuccess) done[dev] = 1;
+  if (cudaMemcpyToSymbolAsync(c_pk_negzero, &nz, sizeof(nz), 0, cudaMemcpyHostToDevice,
+                              stream) == cudaSuccess &&
+      cudaStreamSynchronize(stream) == cudaSuccess)
+    done[dev] = 1;
 }
 
 struct __align__(8) pk {
