@@ -209,17 +209,24 @@ __global__ void __launch_bounds__(32 * NW, MB)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int SX = (int)g.S[0], SY = (int)g.S[1];
   const int G = gridDim.x;
+  // programmatic dependent launch: the next step's grid may be scheduled now; it
+  // waits (griddepcontrol.wait below) until this grid has completed and flushed
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) mbar_init(&bar[k], 1);
+    fence_barrier_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  // everything above overlaps the previous kernel's tail; nothing it wrote
+  // (state, ghosts, CFL slots) is read before this point
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   Coef<T> kc;
   if (!step_coef(a, kc)) return;
   const bool ws = a.cf.dev != nullptr;
   const T gam = (T)a.cf.gamma;
   T wmax = T(0);
   const T gm1 = a.gm1, qx = kc.q[0], nqx = kc.nq2[0], qy = kc.q[1], nqy = kc.nq2[1];
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NS; ++k) mbar_init(&bar[k], 1);
-    fence_barrier_init();
-  }
   __syncthreads();
   auto issue = [&](int i) {
     const int tile = blockIdx.x + i * G;
@@ -444,8 +451,8 @@ static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   const int nsm = sm_count();
   int grid = per_sm * nsm;
   if (grid > ntiles) grid = ntiles;
-  k_step2d_pt<T, V, NW, MB, NS><<<grid, 32 * NW, SM::bytes(), s>>>(
-      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
+  launch_pdl(k_step2d_pt<T, V, NW, MB, NS>, grid, 32 * NW, SM::bytes(), s, a,
+             *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
 }
 
 // ---------------------------------------------------------------------------
