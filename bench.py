@@ -518,7 +518,7 @@ def main():
     peak, peak_src = measured_peak_gbs()
     alg_bytes = 2 * C * elem * local_cells  # per step-kernel launch (one partition per rank)
     kname = {"fused": {1: "k_sweep", 2: "k_step2d_pt",
-                       3: "k_step3d_ra" if wl["dtype"] == "f32" else "k_step3d"}[D],
+                       3: "k_step3d_ra"}[D],
              "split": "k_sweep"}[args.kernel]
     if wl.get("order", 1) == 2:
         kname = {2: "k_step2d_o2", 3: "k_step2d_o2<3> (x-y) + k_zmarch2 (z)"}.get(D, "k_sweep2") \

@@ -519,27 +519,29 @@ __global__ void __launch_bounds__(32 * NW, MB)
 // 2w go through shared memory (half the hand-off traffic of k_step3d_rp).  Same
 // per-cell and per-face operations: bitwise equal to k_step3d / k_sweep.
 // ------------------------------------------------------------------------
-template <int NW>
+template <int NW, typename T = float>
 struct SmemRA {
   static constexpr int W = 32, R = 2 * NW, C = 5, NS = 2;
-  static constexpr int AL = 4;
+  static constexpr int AL = 16 / (int)sizeof(T);
   static constexpr int WB = W + AL;
   static constexpr int STAGE = R * C * WB;
   static constexpr int XY = NW * 2 * C * W;  // (U*, F_y) of row 2w+1, per warp
   static constexpr int FY = NW * C * W;      // face below row 2w, per warp
-  static constexpr size_t bytes() { return (size_t)(NS * STAGE + XY + FY) * 4 + 64; }
+  static constexpr size_t bytes() { return (size_t)(NS * STAGE + XY + FY) * sizeof(T) + 64; }
 };
 
-template <int NW, int MB, int L>
+// P = pk (fp32, packed FFMA2) or pd (fp64, a plain pair of scalar lanes)
+template <int NW, int MB, int L, typename P = pk>
 __global__ void __launch_bounds__(32 * NW, MB)
-    k_step3d_ra(const __grid_constant__ KArgs<float> a, const __grid_constant__ CUtensorMap tmap,
-                int nwin, int nyb) {
+    k_step3d_ra(const __grid_constant__ KArgs<typename PairElem<P>::T> a,
+                const __grid_constant__ CUtensorMap tmap, int nwin, int nyb) {
+  using T = typename PairElem<P>::T;
   constexpr int D = 3, C = 5, W = 32, R = 2 * NW, TY = R - 2;
-  using SM = SmemRA<NW>;
+  using SM = SmemRA<NW, T>;
   extern __shared__ __align__(1024) unsigned char smem[];
-  float* stage = reinterpret_cast<float*>(smem);
-  float* xy = stage + SM::NS * SM::STAGE;
-  float* fyb = xy + SM::XY;
+  T* stage = reinterpret_cast<T*>(smem);
+  T* xy = stage + SM::NS * SM::STAGE;
+  T* fyb = xy + SM::XY;
   uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + SM::FY);
   const Geom& g = a.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -565,11 +567,11 @@ __global__ void __launch_bounds__(32 * NW, MB)
   const bool st1 = out_x & (j1 <= TY) & (yr1 < SY);
   const bool yface0 = (yr0 < g.pad) | (yr0 >= SY - g.pad);
   const bool yface1 = (yr1 < g.pad) | (yr1 >= SY - g.pad);
-  Coef<float> kc;
+  Coef<T> kc;
   if (!step_coef(a, kc)) return;
   const bool ws = a.cf.dev != nullptr;
-  const float gam = (float)a.cf.gamma;
-  float wmax = 0.0f;
+  const T gam = (T)a.cf.gamma;
+  T wmax = T(0);
 
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -583,7 +585,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
   auto issue = [&](int kz) {
     if (kz >= nplanes) return;
     const int s = kz % SM::NS;
-    mbar_arrive_expect_tx(&bar[s], SM::STAGE * 4u);
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
     tma_load_4d(stage + s * SM::STAGE, &tmap, &bar[s], L == 0 ? tx : tx * C, 0, ty,
                 (int)(g.off[2] + z0 - 1 + kz));
   };
@@ -592,13 +594,13 @@ __global__ void __launch_bounds__(32 * NW, MB)
     for (int s = 0; s < SM::NS; ++s) issue(s);
   }
 
-  pk zus[C], zfz[C], zph[C];
+  P zus[C], zfz[C], zph[C];
   int bad = 0, nan = 0;
-  const pk gm1(a.gm1);
-  const pk qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]), nqy(kc.nq2[1]), qz(kc.q[2]), nqz(kc.nq2[2]);
+  const P gm1(a.gm1);
+  const P qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]), nqy(kc.nq2[1]), qz(kc.q[2]), nqz(kc.nq2[2]);
   const int64_t plane = g.rstride * g.P[1], cs = g.cstride;
-  float* dst0 = a.out + g.row(yr0, z0 - 1) * g.rstride + (g.xo + xs) * g.xstride;
-  float* dst1 = a.out + g.row(yr1, z0 - 1) * g.rstride + (g.xo + xs) * g.xstride;
+  T* dst0 = a.out + g.row(yr0, z0 - 1) * g.rstride + (g.xo + xs) * g.xstride;
+  T* dst1 = a.out + g.row(yr1, z0 - 1) * g.rstride + (g.xo + xs) * g.xstride;
   // row 2w-1 lives in warp w-1's slot (warp 0: its own slot, value unused)
   const int wdn = max(warp - 1, 0), wup = min(warp + 1, NW - 1);
 
@@ -606,21 +608,21 @@ __global__ void __launch_bounds__(32 * NW, MB)
     const int z = z0 - 1 + kz;
     const int s = kz % SM::NS;
     mbar_wait(&bar[s], (kz / SM::NS) & 1);
-    pk U[C], F[C], S_[C], G[C];
+    P U[C], F[C], S_[C], G[C];
     {
       constexpr int cst = L == 0 ? SM::WB : 1;
       const int xo = L == 0 ? sh + lane : (sh + lane) * C;
-      const float* r0 = stage + s * SM::STAGE + j0 * C * SM::WB + xo;
-      const float* r1 = stage + s * SM::STAGE + j1 * C * SM::WB + xo;
+      const T* r0 = stage + s * SM::STAGE + j0 * C * SM::WB + xo;
+      const T* r1 = stage + s * SM::STAGE + j1 * C * SM::WB + xo;
 #pragma unroll
-      for (int c = 0; c < C; ++c) U[c] = pk(r0[c * cst], r1[c * cst]);
+      for (int c = 0; c < C; ++c) U[c] = P(r0[c * cst], r1[c * cst]);
     }
     {
       const PkDom b = phys_flux<D, 0>(U, F, gm1);
       bad |= (in0 ? b.a : 0) | (in1 ? b.b : 0);
     }
     {
-      pk Un[C], Fn[C], Pnx[C];
+      P Un[C], Fn[C], Pnx[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         Un[c] = shfl_down1(U[c]);
@@ -635,7 +637,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
       bad |= (ok0 ? b.a : 0) | (ok1 ? b.b : 0);
     }
     {
-      float* x1 = xy + warp * 2 * C * W + lane;  // row 2w+1 for warp w+1
+      T* x1 = xy + warp * 2 * C * W + lane;  // row 2w+1 for warp w+1
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         x1[c * W] = S_[c].y;
@@ -648,71 +650,71 @@ __global__ void __launch_bounds__(32 * NW, MB)
       issue(kz + SM::NS);
     }
     // ---------------- Y: faces (2w-1 | 2w) and (2w | 2w+1) in one packed evaluation
-    pk Py[C];
+    P Py[C];
     {
-      const float* pd = xy + wdn * 2 * C * W + lane;
-      pk SL[C], GL[C], SR[C], GR[C];
+      const T* pdn = xy + wdn * 2 * C * W + lane;
+      P SL[C], GL[C], SR[C], GR[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        SL[c] = pk(pd[c * W], S_[c].x);
-        GL[c] = pk(pd[(C + c) * W], G[c].x);
-        SR[c] = pk(S_[c].x, S_[c].y);
-        GR[c] = pk(G[c].x, G[c].y);
+        SL[c] = P(pdn[c * W], S_[c].x);
+        GL[c] = P(pdn[(C + c) * W], G[c].x);
+        SR[c] = P(S_[c].x, S_[c].y);
+        GR[c] = P(G[c].x, G[c].y);
       }
       force_face<D, 1>(SL, GL, SR, GR, Py, qy, nqy, gm1);
-      float* f0 = fyb + warp * C * W + lane;  // face below row 2w, for warp w-1
+      T* f0 = fyb + warp * C * W + lane;  // face below row 2w, for warp w-1
 #pragma unroll
       for (int c = 0; c < C; ++c) f0[c * W] = Py[c].x;
     }
     __syncthreads();  // (B)
     {
-      const float* fu = fyb + wup * C * W + lane;  // face below row 2w+2 (warp w+1)
-      pk Us[C], Gz[C];
+      const T* fu = fyb + wup * C * W + lane;  // face below row 2w+2 (warp w+1)
+      P Us[C], Gz[C];
 #pragma unroll
       for (int c = 0; c < C; ++c)
-        Us[c] = S_[c] - (pk(Py[c].y, fu[c * W]) - pk(Py[c].x, Py[c].y));
+        Us[c] = S_[c] - (P(Py[c].y, fu[c * W]) - P(Py[c].x, Py[c].y));
       {
         const PkDom b = phys_flux<D, 2>(Us, Gz, gm1);
         bad |= (st0 ? b.a : 0) | (st1 ? b.b : 0);
       }
       if (kz >= 1) {
-        pk Pz[C];
+        P Pz[C];
         force_face<D, 2>(zus, zfz, Us, Gz, Pz, qz, nqz, gm1);
         if (kz >= 2) {
-          pk o[C];
+          P o[C];
 #pragma unroll
           for (int c = 0; c < C; ++c) o[c] = zus[c] - (Pz[c] - zph[c]);
           dst0 += plane;
           dst1 += plane;
           const bool zf = (z - 1 < g.pad) | (z - 1 >= SZ - g.pad);
           if (st0) {
-            float v[C];
+            T v[C];
 #pragma unroll
             for (int c = 0; c < C; ++c) v[c] = o[c].x;
             nan = max(nan, max(naninf(v[0]), naninf(v[C - 1])));
-            if (ws) wmax = fmaxf(wmax, wavespeed<D>(v, a.gm1, gam));
+            if (ws) wmax = fmax(wmax, wavespeed<D>(v, a.gm1, gam));
 #pragma unroll
             for (int c = 0; c < C; ++c) dst0[c * cs] = v[c];
             if (xface | yface0 | zf) {
               if (g.img_fast)
                 images_single<D>(g, a.out, xs, yr0, z - 1, v);
               else
-                images3_nl<D, L, float>(&a, xs, yr0, z - 1, v[0], v[1], v[2], v[3], v[4]);
+                images3_nl<D, L, T>(&a, xs, yr0, z - 1, v[0], v[1], v[2], v[3], v[4]);
             }
           }
           if (st1) {
-            float v[C];
+            T v[C];
 #pragma unroll
             for (int c = 0; c < C; ++c) v[c] = o[c].y;
             nan = max(nan, max(naninf(v[0]), naninf(v[C - 1])));
-            if (ws) wmax = fmaxf(wmax, wavespeed<D>(v, a.gm1, gam));
+            if (ws) wmax = fmax(wmax, wavespeed<D>(v, a.gm1, gam));
 #pragma unroll
             for (int c = 0; c < C; ++c) dst1[c * cs] = v[c];
             if (xface | yface1 | zf) {
               if (g.img_fast)
                 images_single<D>(g, a.out, xs, yr1, z - 1, v);
               else
-                images3_nl<D, L, float>(&a, xs, yr1, z - 1, v[0], v[1], v[2], v[3], v[4]);
+                images3_nl<D, L, T>(&a, xs, yr1, z - 1, v[0], v[1], v[2], v[3], v[4]);
             }
           }
         }
@@ -726,7 +728,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
       }
     }
   }
-  if (__any_sync(0xffffffffu, bad < 0 || nan >= kExpMask<float>) && lane == 0) atomicOr(a.flag, 1u);
+  if (__any_sync(0xffffffffu, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
   if (ws) publish_max(a, wmax);
 }
 
@@ -786,18 +788,20 @@ static int win3(const Geom& g, int variant) {
   return (g.elem == 4 && variant == 21) ? 64 : 32;
 }
 
-template <int NW, int MB, int L>
-static int launch3_ra(const KArgs<float>& a, const void* tmap, cudaStream_t s) {
+template <int NW, int MB, int L, typename P = pk>
+static int launch3_ra(const KArgs<typename PairElem<P>::T>& a, const void* tmap,
+                      cudaStream_t s) {
+  using T = typename PairElem<P>::T;
   constexpr int W = 32, TY = 2 * NW - 2;
   const Geom& g = a.g;
   const int nwin = (int)((g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((g.S[1] + TY - 1) / TY);
   const int nzc = (int)((g.S[2] + a.rows - 1) / a.rows);
-  const size_t sm = SmemRA<NW>::bytes();
-  pk_set_negzero(s);
+  const size_t sm = SmemRA<NW, T>::bytes();
+  if constexpr (sizeof(T) == 4) pk_set_negzero(s);
   static int cache[kMaxDevices] = {0};
-  resident_ctas(k_step3d_ra<NW, MB, L>, 32 * NW, sm, cache);
-  k_step3d_ra<NW, MB, L><<<nwin * nyb * nzc, 32 * NW, sm, s>>>(
+  resident_ctas(k_step3d_ra<NW, MB, L, P>, 32 * NW, sm, cache);
+  k_step3d_ra<NW, MB, L, P><<<nwin * nyb * nzc, 32 * NW, sm, s>>>(
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb);
   return 0;
 }
@@ -865,6 +869,12 @@ int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
       return a.g.layout == 1 ? launch3_ra<8, 2, 1>(a, tmap, s) : launch3_ra<8, 2, 0>(a, tmap, s);
     }
   }
+  if constexpr (sizeof(T) == 8) {
+    // fp64 default: adjacent row pairs, two scalar rows per lane (k_step3d_ra<pd>, 8
+    // warps, 216 registers, 1 CTA/SM): 512^3 4340 us vs 4533 us for k_step3d (56)
+    if (a.variant == 0)
+      return a.g.layout == 1 ? launch3_ra<8, 1, 1, pd>(a, tmap, s) : launch3_ra<8, 1, 0, pd>(a, tmap, s);
+  }
   if (a.g.layout == 1) return launch3<T, 1, 14, 1, 1>(a, tmap, s);  // AoS (configs[4])
   if constexpr (sizeof(T) == 4) {
     // V = 2 (two cells per lane) only for fp32 -- must match win3() / the TMA box
@@ -874,6 +884,7 @@ int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 50: return launch3<T, 1, 30>(a, tmap, s);
     case 51: return launch3<T, 1, 22>(a, tmap, s);
     case 52: return launch3<T, 1, 14, 2>(a, tmap, s);
+    case 56: return launch3<T, 1, 14>(a, tmap, s);  // fp64: the one-row-per-warp kernel
     default: return launch3<T, 1, 14>(a, tmap, s);
   }
 }

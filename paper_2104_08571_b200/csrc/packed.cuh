@@ -97,6 +97,39 @@ __device__ __forceinline__ PkDom dom_word(pk rho, pk p) {
   return PkDom{dom_word(rho.x, p.x), dom_word(rho.y, p.y)};
 }
 
+// fp64 counterpart: two cells' values of one component as a plain pair (no packed
+// FP64 instructions exist); lets the row-pair kernels run in double precision with
+// exactly the scalar operations (mul stays a DMUL under -fmad=false).
+struct pd {
+  double x, y;
+  __device__ __forceinline__ pd() {}
+  __device__ __forceinline__ pd(double a, double b) : x(a), y(b) {}
+  template <typename S>
+  __device__ __forceinline__ explicit pd(S s) : x((double)s), y((double)s) {}
+};
+__device__ __forceinline__ pd operator+(pd a, pd b) { return pd(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ pd operator-(pd a, pd b) { return pd(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ pd operator*(pd a, pd b) { return pd(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ pd operator-(pd a) { return pd(-a.x, -a.y); }
+__device__ __forceinline__ pd fma(pd a, pd b, pd c) {
+  return pd(::fma(a.x, b.x, c.x), ::fma(a.y, b.y, c.y));
+}
+__device__ __forceinline__ pd rcp(pd a) { return pd(rcp(a.x), rcp(a.y)); }
+__device__ __forceinline__ PkDom dom_word(pd rho, pd p) {
+  return PkDom{dom_word(rho.x, p.x), dom_word(rho.y, p.y)};
+}
+__device__ __forceinline__ pd shfl_down1(pd v) {
+  return pd(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+}
+__device__ __forceinline__ pd shfl_up1(pd v) {
+  return pd(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+}
+
+// element type of a pair type
+template <typename P> struct PairElem;
+template <> struct PairElem<pk> { using T = float; };
+template <> struct PairElem<pd> { using T = double; };
+
 __device__ __forceinline__ pk shfl_down1(pk v) {
   return pk(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
 }

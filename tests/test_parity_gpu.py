@@ -471,12 +471,13 @@ def test_full_size_sampled_flux_difference_fd8k():
 
 
 @pytest.mark.parametrize("variant,dtype", [("0", "f32"), ("20", "f32"), ("21", "f32"),
-                                           ("70", "f32"), ("78", "f32"), ("21", "f64"), ("51", "f64"),
+                                           ("70", "f32"), ("78", "f32"), ("56", "f64"), ("21", "f64"), ("51", "f64"),
                                            ("51", "f32")])
 def test_3d_kernel_variants_bitwise(variant, dtype, monkeypatch):
     """3-D fused variants (RPL_VARIANT: 0 = default, for fp32 the packed adjacent
     row-pair kernel (FFMA2, in-register y-face, 8 warps / 14 rows); 78 = packed
-    rows w, w+8; 70 = the same, 16 warps / 30 rows;
+    rows w, w+8; 70 = the same, 16 warps / 30 rows; for fp64 the default is the
+    adjacent row-pair kernel with scalar pairs, 56 = one row per warp;
     20 = scalar one cell per lane; 21 = two cells per lane for fp32, the default
     for fp64; 51 = 22-row tiles) give bitwise the split kernel's result (ragged
     windows, tiles and z-chunks)."""
