@@ -517,7 +517,7 @@ def main():
         launches_per_step = 1
     peak, peak_src = measured_peak_gbs()
     alg_bytes = 2 * C * elem * local_cells  # per step-kernel launch (one partition per rank)
-    kname = {"fused": {1: "k_sweep", 2: "k_step2d_pt",
+    kname = {"fused": {1: "k_sweep", 2: "k_step2d_ra",
                        3: "k_step3d_ra"}[D],
              "split": "k_sweep"}[args.kernel]
     if wl.get("order", 1) == 2:

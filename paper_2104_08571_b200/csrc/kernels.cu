@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "async.cuh"
 #include "launch.cuh"
 #include "kernels.hpp"
@@ -796,7 +798,8 @@ int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
     case 33: v = 2; nw = 16; break;
     case 36: v = 2; nw = 8; break;
     case 38: nw = 10; break;
-    case 44: case 45: nw = 24; break;
+    case 44: case 45: case 64: nw = 24; break;
+    case 63: case 65: case 66: nw = 12; break;
     case 46: nw = 14; break;
     case 47: nw = 20; break;
     default: nw = 12; break;  // 0, 37, 39
@@ -952,14 +955,199 @@ int auto_rows_3d(const Geom& g) {
   return (int)rows;
 }
 
-// Default 2-D order-1 tile shape.  12-row tiles, 2 CTAs/SM (variant 0/37) at
-// small partitions, where their finer granularity shortens the last wave (1024^2:
-// 28.9 us vs 29.9 us for 24-row tiles); 24-row tiles, 1 CTA/SM, 3-stage ring
-// (variant 45: 10 of 12 vs 22 of 24 rows are outputs) once a partition has >= 32
-// such tiles per SM (6400x4000: 450 us vs 475 us; profiles/r1/tile_shape_2d.txt).
+
+// ---------------------------------------------------------------------------
+// K-B (2-D), adjacent row pairs: warp w owns tile rows 2w and 2w+1 (P = pd: two
+// scalar doubles; P = pk: packed fp32), so the y-face between them is evaluated
+// in registers together with the face below row 2w, and only row 2w+1's (U*, F_y)
+// and that lower face go through shared memory.  Same tile walk, TMA ring and
+// per-cell / per-face operations as k_step2d_pt: bitwise equal.
+// ---------------------------------------------------------------------------
+template <typename P, int NW, int MB, int NS>
+__global__ void __launch_bounds__(32 * NW, MB)
+    k_step2d_ra(const __grid_constant__ KArgs<typename PairElem<P>::T> a,
+                const __grid_constant__ CUtensorMap tmap, int nwin, int ntiles) {
+  using T = typename PairElem<P>::T;
+  constexpr int D = 2, C = 4, W = 32, R = 2 * NW;
+  constexpr int AL = 16 / (int)sizeof(T), WB = W + AL, STAGE = R * C * WB;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  T* stage = reinterpret_cast<T*>(smem);
+  T* xy = stage + NS * STAGE;          // (U*, F_y) of row 2w+1, per warp
+  T* fy = xy + NW * 2 * C * W;         // face below row 2w, per warp
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fy + NW * C * W);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = 2 * warp, j1 = 2 * warp + 1;
+  const int wdn = max(warp - 1, 0), wup = min(warp + 1, NW - 1);
+  const int SX = (int)g.S[0], SY = (int)g.S[1];
+  const int G = gridDim.x;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) mbar_init(&bar[k], 1);
+    fence_barrier_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  Coef<T> kc;
+  if (!step_coef(a, kc)) return;
+  const bool ws = a.cf.dev != nullptr;
+  const T gam = (T)a.cf.gamma;
+  T wmax = T(0);
+  const P gm1(a.gm1), qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]), nqy(kc.nq2[1]);
+  __syncthreads();
+  auto issue = [&](int i) {
+    const int tile = blockIdx.x + i * G;
+    if (tile >= ntiles) return;
+    const int s = i % NS;
+    const int w = tile % nwin, yb = tile / nwin;
+    mbar_arrive_expect_tx(&bar[s], STAGE * (unsigned)sizeof(T));
+    const int x0 = (int)g.xo + w * (W - 2) - 1;
+    tma_load_box(stage + s * STAGE, &tmap, &bar[s], x0 - x0 % AL, 0,
+                 (int)g.off[1] + yb * (R - 2) - 1, 0);
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) issue(k);
+  }
+  int bad = 0, nan = 0;
+  const unsigned bar_a0 = smem_u32(&bar[0]);
+  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
+  int win = (int)blockIdx.x % nwin, yb = (int)blockIdx.x / nwin;
+  const int nyb = ntiles / nwin;
+  const int64_t cs = g.cstride;
+  for (int i = 0;; ++i) {
+    if (yb >= nyb) break;
+    const int xw = win * (W - 2) - 1;
+    const int yr0 = yb * (R - 2) - 1 + j0, yr1 = yr0 + 1;
+    const int xv = xw + lane;
+    const bool in_x = (xv >= -1) & (xv <= SX);
+    const bool out_x = (lane >= 1) & (lane <= W - 2) & (xv < SX);
+    const int s = NS == 2 ? (i & 1) : i % NS;
+    mbar_wait_u32(bar_a0 + 8 * s, (i / NS) & 1);
+    // ---- X (both rows)
+    P U[C], F[C], S_[C], G_[C];
+    {
+      const int sh = ((int)g.xo + xw) % AL;
+      const T* r0 = stage + s * STAGE + j0 * C * WB + sh + lane;
+      const T* r1 = r0 + C * WB;
+#pragma unroll
+      for (int c = 0; c < C; ++c) U[c] = P(r0[c * WB], r1[c * WB]);
+    }
+    {
+      const PkDom b = phys_flux<D, 0>(U, F, gm1);
+      bad |= ((in_x & (yr0 <= SY)) ? b.a : 0) | ((in_x & (yr1 <= SY)) ? b.b : 0);
+    }
+    {
+      P Un[C], Fn[C], Pnx[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Un[c] = shfl_down1(U[c]);
+        Fn[c] = shfl_down1(F[c]);
+      }
+      force_face<D, 0>(U, F, Un, Fn, Pnx, qx, nqx, gm1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) S_[c] = U[c] - (Pnx[c] - shfl_up1(Pnx[c]));
+    }
+    {
+      const PkDom b = phys_flux<D, 1>(S_, G_, gm1);
+      bad |= ((out_x & (yr0 <= SY)) ? b.a : 0) | ((out_x & (yr1 <= SY)) ? b.b : 0);
+    }
+    {
+      T* x1 = xy + warp * 2 * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        x1[c * W] = S_[c].y;
+        x1[(C + c) * W] = G_[c].y;
+      }
+    }
+    __syncthreads();  // (A) stage s consumed; row 2w+1 published
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      issue(i + NS);
+    }
+    // ---- Y faces (2w-1 | 2w) and (2w | 2w+1), one pair evaluation
+    P Py[C];
+    {
+      const T* pdn = xy + wdn * 2 * C * W + lane;
+      P SL[C], GL[C], SR[C], GR[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        SL[c] = P(pdn[c * W], S_[c].x);
+        GL[c] = P(pdn[(C + c) * W], G_[c].x);
+        SR[c] = P(S_[c].x, S_[c].y);
+        GR[c] = P(G_[c].x, G_[c].y);
+      }
+      force_face<D, 1>(SL, GL, SR, GR, Py, qy, nqy, gm1);
+      T* f0 = fy + warp * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) f0[c * W] = Py[c].x;
+    }
+    __syncthreads();  // (B) faces below each pair published
+    // ---- update + store
+    {
+      const T* fu = fy + wup * C * W + lane;  // face below row 2w+2
+      P o[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) o[c] = S_[c] - (P(Py[c].y, fu[c * W]) - P(Py[c].x, Py[c].y));
+      const bool st0 = out_x & (j0 >= 1) & (yr0 < SY);
+      const bool st1 = out_x & (j1 <= R - 2) & (yr1 < SY);
+      const bool xface = (xv < g.pad) | (xv >= SX - g.pad);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool st = h ? st1 : st0;
+        if (!st) continue;
+        const int yr = h ? yr1 : yr0;
+        T v[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[c] = h ? o[c].y : o[c].x;
+        T* dst = a.out + ((int64_t)((int)g.off[1] + yr) * g.rstride + (int)g.xo + xv);
+#pragma unroll
+        for (int c = 0; c < C; ++c) dst[c * cs] = v[c];
+        nan = max(nan, max(naninf(v[0]), naninf(v[C - 1])));
+        if (ws) wmax = fmax(wmax, wavespeed<D>(v, a.gm1, gam));
+        if (xface | (yr < g.pad) | (yr >= SY - g.pad)) images<D, 0>(a, xv, yr, 0, v);
+      }
+    }
+    win += Gr;
+    yb += Gq;
+    if (win >= nwin) {
+      win -= nwin;
+      ++yb;
+    }
+  }
+  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
+}
+
+template <typename P, int NW, int MB, int NS>
+static void launch_ra2d(const KArgs<typename PairElem<P>::T>& a, const void* tmap,
+                        cudaStream_t s) {
+  using T = typename PairElem<P>::T;
+  constexpr int W = 32, R = 2 * NW, C = 4, AL = 16 / (int)sizeof(T);
+  const size_t bytes = (size_t)(NS * R * C * (W + AL) + NW * 3 * C * W) * sizeof(T) + 64;
+  const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
+  const int nyb = (int)((a.g.S[1] + (R - 2) - 1) / (R - 2));
+  const int ntiles = nwin * nyb;
+  if constexpr (sizeof(T) == 4) pk_set_negzero(s);
+  static int cache[kMaxDevices] = {0};
+  const int per_sm = resident_ctas(k_step2d_ra<P, NW, MB, NS>, 32 * NW, bytes, cache);
+  int grid = per_sm * sm_count();
+  if (grid > ntiles) grid = ntiles;
+  launch_pdl(k_step2d_ra<P, NW, MB, NS>, grid, 32 * NW, bytes, s, a,
+             *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
+}
+
+// Default 2-D order-1 kernel: adjacent row pairs (k_step2d_ra).  12-row tiles of
+// 6 warps, 4 CTAs/SM (variant 66) at small partitions, where the finer granularity
+// shortens the last wave (1024^2: 27.1 us vs 29.1 us for k_step2d_pt); 24-row
+// tiles of 12 warps, 1 CTA/SM, 3-stage ring (variant 64: 22 of 24 rows are
+// outputs) once a partition has >= 32 such tiles per SM (6400x4000: 414 us vs
+// 451 us for k_step2d_pt variant 45; profiles/r1/tile_shape_2d.txt,
+// profiles/r1/ra2d_variants.txt).
 int auto_variant_2d(const Geom& g) {
   const int64_t tiles24 = ((g.S[0] + 29) / 30) * ((g.S[1] + 21) / 22);
-  return tiles24 >= 32LL * sm_count() ? 45 : 0;
+  return tiles24 >= 32LL * sm_count() ? 64 : 66;
 }
 
 template <typename T>
@@ -982,6 +1170,10 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 48: return launch_pt2d<T, 1, 12, 2, 3>(a, tmap, s);  // 3-stage TMA ring
     case 49: return launch_pt2d<T, 1, 12, 2, 4>(a, tmap, s);  // 4-stage TMA ring
     case 45: return launch_pt2d<T, 1, 24, 1, 3>(a, tmap, s);
+    case 63: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 6, 2, 2>(a, tmap, s);
+    case 64: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 12, 1, 3>(a, tmap, s);
+    case 65: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 6, 3, 2>(a, tmap, s);
+    case 66: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 6, 4, 2>(a, tmap, s);
     default: return launch_pt2d<T, 1, 12, 2>(a, tmap, s);  // 0 / 37: the default
   }
 }

@@ -8,5 +8,5 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')
 timeout 600 python bench.py > $OUT/bench_2d1024.json 2>$OUT/bench_err.log
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_reference.json 2>>$OUT/bench_err.log
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_2d1024.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_step2d_pt -s 3 -c 1 -o $OUT/step2d python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $OUT/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_step2d_ra -s 3 -c 1 -o $OUT/step2d python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $OUT/ncu_full.log 2>&1
 tail -3 $OUT/pytest_gpu.log; cat $OUT/smoke.log | tail -1; cat $OUT/bench_2d1024.json | tail -1 | cut -c1-400

@@ -10,7 +10,7 @@ cap() { name=$1; regex=$2; shift 2; timeout 900 ncu --set full --clock-control n
   rm -f $OUT/$name.ncu-rep; }
 cap w384 k_step3d --workload w384 --steps 2
 cap s512 k_step3d --workload s512 --steps 2
-cap p6400 k_step2d_pt --workload p6400 --steps 2
+cap p6400 k_step2d_ra --workload p6400 --steps 2
 cap o2_1024 k_step2d_o2 --workload o2_1024 --steps 3
 cap o2_s256_xy k_step2d_o2 --workload o2_s256 --steps 2
 cap o2_s256_z k_zmarch2 --workload o2_s256 --steps 2
@@ -20,5 +20,5 @@ cap l256_f32_soa k_step3d --workload l256 --dtype f32 --steps 2
 cap l256_f32_aos k_step3d --workload l256 --dtype f32 --layout aos --steps 2
 cap l256_f64_soa k_step3d --workload l256 --dtype f64 --steps 2
 cap l256_f64_aos k_step3d --workload l256 --dtype f64 --layout aos --steps 2
-cap cfl1024 k_step2d_pt --workload cfl1024 --steps 2
+cap cfl1024 k_step2d_ra --workload cfl1024 --steps 2
 ls -la $OUT; cat $OUT/ncu_*.txt
