@@ -1592,16 +1592,17 @@ static void launch_fd_rp(const KArgs<float>& a, const void* tmap, cudaStream_t s
 // between them is computed in registers together with the face below row 2w
 // (one packed force_face); only row 2w+1's (U, F_y) and that lower face go
 // through shared memory.  Same operations per face and cell: bitwise equal.
-template <int NW, int MB>
+template <int NW, int MB, typename P = pk>
 __global__ void __launch_bounds__(32 * NW, MB)
-    k_fluxdiff_ra(const __grid_constant__ KArgs<float> a, const __grid_constant__ CUtensorMap tmap,
-                  int nwin, int ntiles) {
+    k_fluxdiff_ra(const __grid_constant__ KArgs<typename PairElem<P>::T> a,
+                  const __grid_constant__ CUtensorMap tmap, int nwin, int ntiles) {
+  using T = typename PairElem<P>::T;
   constexpr int D = 2, C = 4, W = 32, R = 2 * NW;
-  using SM = SmemFD<float, R>;  // stage geometry of the 2 NW-row box
+  using SM = SmemFD<T, R>;  // stage geometry of the 2 NW-row box
   extern __shared__ __align__(1024) unsigned char smem[];
-  float* stage = reinterpret_cast<float*>(smem);
-  float* uf = stage + 2 * SM::STAGE;
-  float* fyb = uf + NW * 2 * C * W;
+  T* stage = reinterpret_cast<T*>(smem);
+  T* uf = stage + 2 * SM::STAGE;
+  T* fyb = uf + NW * 2 * C * W;
   uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + NW * C * W);
   const Geom& g = a.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1609,9 +1610,9 @@ __global__ void __launch_bounds__(32 * NW, MB)
   const int wdn = max(warp - 1, 0), wup = min(warp + 1, NW - 1);
   const int SX = (int)g.S[0], SY = (int)g.S[1];
   const int G = gridDim.x;
-  const pk gm1(a.gm1);
-  const pk ilx(0.25f / a.q[0]), ily(0.25f / a.q[1]);
-  const pk qx(a.q[0]), nqx(a.nq2[0]), qy(a.q[1]), nqy(a.nq2[1]);
+  const P gm1(a.gm1);
+  const P ilx(T(0.25) / a.q[0]), ily(T(0.25) / a.q[1]);
+  const P qx(a.q[0]), nqx(a.nq2[0]), qy(a.q[1]), nqy(a.nq2[1]);
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -1623,7 +1624,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
     if (tile >= ntiles) return;
     const int s = i & 1;
     const int w = tile % nwin, yb = tile / nwin;
-    mbar_arrive_expect_tx(&bar[s], SM::STAGE * 4u);
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
     const int x0 = (int)g.xo + w * (W - 2) - 1;
     tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
                  (int)g.off[1] + yb * (R - 2) - 1, 0);
@@ -1641,18 +1642,18 @@ __global__ void __launch_bounds__(32 * NW, MB)
     const int yr0 = yb * (R - 2) - 1 + j0, yr1 = yr0 + 1;
     const int s = i & 1;
     mbar_wait(&bar[s], (i >> 1) & 1);
-    pk U[C], Fx[C], Fy[C], Rx[C];
+    P U[C], Fx[C], Fy[C], Rx[C];
     {
       const int sh = ((int)g.xo + xw) % SM::AL;
-      const float* s0 = stage + s * SM::STAGE + j0 * C * SM::WB + sh + lane;
-      const float* s1 = s0 + C * SM::WB;
+      const T* s0 = stage + s * SM::STAGE + j0 * C * SM::WB + sh + lane;
+      const T* s1 = s0 + C * SM::WB;
 #pragma unroll
-      for (int c = 0; c < C; ++c) U[c] = pk(s0[c * SM::WB], s1[c * SM::WB]);
+      for (int c = 0; c < C; ++c) U[c] = P(s0[c * SM::WB], s1[c * SM::WB]);
     }
     phys_flux<D, 0>(U, Fx, gm1);
     phys_flux<D, 1>(U, Fy, gm1);
     {
-      pk Un[C], Fn[C], Pnx[C];
+      P Un[C], Fn[C], Pnx[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         Un[c] = shfl_down1(U[c]);
@@ -1660,10 +1661,10 @@ __global__ void __launch_bounds__(32 * NW, MB)
       }
       force_face<D, 0>(U, Fx, Un, Fn, Pnx, qx, nqx, gm1);
 #pragma unroll
-      for (int c = 0; c < C; ++c) Rx[c] = fma(Pnx[c] - shfl_up1(Pnx[c]), ilx, pk(0.0f));
+      for (int c = 0; c < C; ++c) Rx[c] = fma(Pnx[c] - shfl_up1(Pnx[c]), ilx, P(T(0)));
     }
     {
-      float* w1 = uf + warp * 2 * C * W + lane;  // row 2w+1 for warp w+1
+      T* w1 = uf + warp * 2 * C * W + lane;  // row 2w+1 for warp w+1
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         w1[c * W] = U[c].y;
@@ -1675,19 +1676,19 @@ __global__ void __launch_bounds__(32 * NW, MB)
       fence_proxy_async();
       issue(i + 2);
     }
-    pk Py[C];
+    P Py[C];
     {
-      const float* pd = uf + wdn * 2 * C * W + lane;
-      pk UL[C], FL[C], UR[C], FR[C];
+      const T* pdn = uf + wdn * 2 * C * W + lane;
+      P UL[C], FL[C], UR[C], FR[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        UL[c] = pk(pd[c * W], U[c].x);
-        FL[c] = pk(pd[(C + c) * W], Fy[c].x);
-        UR[c] = pk(U[c].x, U[c].y);
-        FR[c] = pk(Fy[c].x, Fy[c].y);
+        UL[c] = P(pdn[c * W], U[c].x);
+        FL[c] = P(pdn[(C + c) * W], Fy[c].x);
+        UR[c] = P(U[c].x, U[c].y);
+        FR[c] = P(Fy[c].x, Fy[c].y);
       }
       force_face<D, 1>(UL, FL, UR, FR, Py, qy, nqy, gm1);
-      float* f0 = fyb + warp * C * W + lane;  // face below row 2w, for warp w-1
+      T* f0 = fyb + warp * C * W + lane;  // face below row 2w, for warp w-1
 #pragma unroll
       for (int c = 0; c < C; ++c) f0[c * W] = Py[c].x;
     }
@@ -1696,19 +1697,19 @@ __global__ void __launch_bounds__(32 * NW, MB)
       const bool xok = lane >= 1 && lane <= 30 && xw + lane < SX;
       const bool ok0 = xok && j0 >= 1 && yr0 < SY;
       const bool ok1 = xok && j1 <= R - 2 && yr1 < SY;
-      const float* fu = fyb + wup * C * W + lane;  // face below row 2w+2
-      pk o[C];
+      const T* fu = fyb + wup * C * W + lane;  // face below row 2w+2
+      P o[C];
 #pragma unroll
       for (int c = 0; c < C; ++c)
-        o[c] = fma(pk(Py[c].y, fu[c * W]) - pk(Py[c].x, Py[c].y), ily, Rx[c]);
+        o[c] = fma(P(Py[c].y, fu[c * W]) - P(Py[c].x, Py[c].y), ily, Rx[c]);
       const int64_t cs = g.cstride;
       if (ok0) {
-        float* dst = a.out + ((int64_t)((int)g.off[1] + yr0) * g.rstride + (int)g.xo + xw + lane);
+        T* dst = a.out + ((int64_t)((int)g.off[1] + yr0) * g.rstride + (int)g.xo + xw + lane);
 #pragma unroll
         for (int c = 0; c < C; ++c) dst[c * cs] = o[c].x;
       }
       if (ok1) {
-        float* dst = a.out + ((int64_t)((int)g.off[1] + yr1) * g.rstride + (int)g.xo + xw + lane);
+        T* dst = a.out + ((int64_t)((int)g.off[1] + yr1) * g.rstride + (int)g.xo + xw + lane);
 #pragma unroll
         for (int c = 0; c < C; ++c) dst[c * cs] = o[c].y;
       }
@@ -1722,21 +1723,23 @@ __global__ void __launch_bounds__(32 * NW, MB)
   }
 }
 
-template <int NW, int MB>
-static void launch_fd_ra(const KArgs<float>& a, const void* tmap, cudaStream_t s) {
+template <int NW, int MB, typename P = pk>
+static void launch_fd_ra(const KArgs<typename PairElem<P>::T>& a, const void* tmap,
+                         cudaStream_t s) {
+  using T = typename PairElem<P>::T;
   constexpr int W = 32, R = 2 * NW, C = 4;
-  using SM = SmemFD<float, R>;
-  const size_t bytes = (size_t)(2 * SM::STAGE + NW * 3 * C * W) * 4 + 64;
+  using SM = SmemFD<T, R>;
+  const size_t bytes = (size_t)(2 * SM::STAGE + NW * 3 * C * W) * sizeof(T) + 64;
   const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((a.g.S[1] + (R - 2) - 1) / (R - 2));
   const int ntiles = nwin * nyb;
-  pk_set_negzero(s);
+  if constexpr (sizeof(T) == 4) pk_set_negzero(s);
   static int cache[kMaxDevices] = {0};
-  const int per_sm = resident_ctas(k_fluxdiff_ra<NW, MB>, 32 * NW, bytes, cache);
+  const int per_sm = resident_ctas(k_fluxdiff_ra<NW, MB, P>, 32 * NW, bytes, cache);
   const int nsm = sm_count();
   int grid = per_sm * nsm;
   if (grid > ntiles) grid = ntiles;
-  k_fluxdiff_ra<NW, MB><<<grid, 32 * NW, bytes, s>>>(
+  k_fluxdiff_ra<NW, MB, P><<<grid, 32 * NW, bytes, s>>>(
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
 }
 
@@ -1752,7 +1755,11 @@ void launch_fluxdiff_tiled(const KArgs<T>& a, const void* tmap, cudaStream_t s) 
     if (a.variant == 78) return launch_fd_rp<8, 4>(a, tmap, s);
     return launch_fd_ra<8, 4>(a, tmap, s);  // adjacent row pairs (default)
   }
-  return launch_fd_pt<T, 16, 2>(a, tmap, s);
+  if constexpr (sizeof(T) == 8) {
+    if (a.variant == 20) return launch_fd_pt<T, 16, 2>(a, tmap, s);  // fp64 scalar tiles
+    if (a.variant == 79) return launch_fd_ra<8, 3, pd>(a, tmap, s);
+    return launch_fd_ra<8, 2, pd>(a, tmap, s);  // fp64 adjacent row pairs (default)
+  }
 }
 template void launch_fluxdiff_tiled<float>(const KArgs<float>&, const void*, cudaStream_t);
 template void launch_fluxdiff_tiled<double>(const KArgs<double>&, const void*, cudaStream_t);

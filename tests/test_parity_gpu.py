@@ -402,6 +402,24 @@ def test_flux_difference_fp32_variants_bitwise(variant, monkeypatch):
     assert bits_equal(out[0], out[1])
 
 
+@pytest.mark.parametrize("variant", ["0", "20", "79"])
+def test_flux_difference_fp64_variants_bitwise(variant, monkeypatch):
+    """f2 fp64 tiled kernels (RPL_VARIANT: 0 = adjacent row pairs of doubles, 8 warps x
+    2 CTAs; 79 = the same, 3 CTAs; 20 = one row per warp) == per-cell kernel."""
+    n = (1000, 333)
+    dx = [1.0 / n[0]] * 2
+    U0 = W.shock_bubble(n, dx=dx)
+    out = []
+    for kernel in ("split", "fused"):
+        if kernel == "fused":
+            monkeypatch.setenv("RPL_VARIANT", variant)
+        with R.Domain(n, pad=1, dtype="f64", dx=dx, kernel=kernel) as dom:
+            dom.set_state(U0)
+            dom.flux_difference(2e-4)
+            out.append(dom.get_flux_difference())
+    assert bits_equal(out[0], out[1])
+
+
 def _sample_boxes(n, size, count, seed):
     """Patch origins: the corners plus seeded interior positions."""
     rng = np.random.default_rng(seed)
