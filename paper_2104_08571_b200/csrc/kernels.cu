@@ -665,12 +665,223 @@ static void launch_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb, ntiles);
 }
 
+
+// Order 2 with adjacent row pairs (P = pd / pk): warp w owns tile rows 2w and
+// 2w+1 of a 2 NW-row tile.  The y-slopes of each row take the partner row from
+// registers (only rows 2w-1 and 2w+2 come from shared memory), the y-face
+// between the two rows is evaluated in registers together with the face below
+// row 2w, and only row 2w+1's evolved upper value and the face below row 2w are
+// handed over.  Same operations per cell and face: bitwise equal to k_step2d_o2.
+template <typename P, int D, int NW, int MB>
+__global__ void __launch_bounds__(32 * NW, MB)
+    k_step2d_o2p(const __grid_constant__ KArgs<typename PairElem<P>::T> a,
+                 const __grid_constant__ CUtensorMap tmap, int nwin, int nyb, int ntiles) {
+  using T = typename PairElem<P>::T;
+  constexpr int C = D + 2, W = 32, R = 2 * NW;
+  using SM = SmemO2<T, R, C>;  // stage geometry of the 2 NW-row box
+  extern __shared__ __align__(1024) unsigned char smem[];
+  T* stage = reinterpret_cast<T*>(smem);
+  T* sx = stage + 2 * SM::STAGE;         // U* of every tile row
+  T* br = sx + R * C * W;                // (Ubar^R_y, F) of row 2w+1, per warp
+  T* fyb = br + NW * 2 * C * W;          // face below row 2w, per warp
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + NW * C * W);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = 2 * warp, j1 = j0 + 1;
+  const int wdn = max(warp - 1, 0), wup = min(warp + 1, NW - 1);
+  const int SX = (int)g.S[0], SY = (int)g.S[1];
+  const int G = gridDim.x;
+  Coef<T> kc;
+  if (!step_coef(a, kc)) return;
+  const bool ws = a.cf.dev != nullptr && a.cf.last;
+  const T gam = (T)a.cf.gamma;
+  T wmax = T(0);
+  const P gm1(a.gm1), h2x(kc.h2[0]), h2y(kc.h2[1]), qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]),
+      nqy(kc.nq2[1]);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int i) {
+    const int tile = blockIdx.x + i * G;
+    if (tile >= ntiles) return;
+    const int s = i & 1;
+    const int w = tile % nwin, r = tile / nwin, yb = r % nyb, zp = r / nyb;
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
+    const int x0 = (int)g.xo + w * (W - 4) - 2;
+    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
+                 (int)g.off[1] + yb * (R - 4) - 2, (int)g.off[2] + zp);
+  };
+  if (threadIdx.x == 0) {
+    issue(0);
+    issue(1);
+  }
+  int bad = 0, nan = 0;
+  const bool lane_in = (lane >= 1) & (lane <= 30);
+  const bool lane_out = (lane >= 2) & (lane <= 29);
+  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
+  int win = (int)blockIdx.x % nwin, yq = (int)blockIdx.x / nwin;
+  const int nyz = ntiles / nwin;
+  const int SZ = (int)g.S[2];
+  // rows of a pair that take part in Y1 (1..R-2), Y2 (2..R-2) and the update (2..R-3)
+  const bool y1a = j0 >= 1, y1b = j1 <= R - 2;
+  const bool y2a = j0 >= 2, y2b = j1 >= 2 && j1 <= R - 2;
+  const bool upa = j0 >= 2 && j0 <= R - 3, upb = j1 >= 2 && j1 <= R - 3;
+  for (int i = 0;; ++i) {
+    if (yq >= nyz) break;
+    const int yb = D == 2 ? yq : yq % nyb;
+    const int zp = D == 2 ? 0 : yq / nyb;
+    const int xw = win * (W - 4) - 2;
+    const int yr0 = yb * (R - 4) - 2 + j0, yr1 = yr0 + 1;
+    const int xv = xw + lane;
+    const int s = i & 1;
+    mbar_wait(&bar[s], (i >> 1) & 1);
+    // ---- X (both rows)
+    P S_[C];
+    {
+      P U[C], Um[C], Up[C];
+      const int sh = ((int)g.xo + xw) % SM::AL;
+      const T* r0 = stage + s * SM::STAGE + j0 * C * SM::WB + sh + lane;
+      const T* r1 = r0 + C * SM::WB;
+#pragma unroll
+      for (int c = 0; c < C; ++c) U[c] = P(r0[c * SM::WB], r1[c * SM::WB]);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Um[c] = shfl_up1(U[c]);
+        Up[c] = shfl_down1(U[c]);
+      }
+      P bL[C], FbL[C], bR[C], FbR[C];
+      const PkDom b = hancock<D, 0>(Um, U, Up, h2x, gm1, bL, FbL, bR, FbR);
+      const bool xin = lane_in & (xv >= -1) & (xv <= SX);
+      bad |= ((xin & (yr0 <= SY + 1)) ? b.a : 0) | ((xin & (yr1 <= SY + 1)) ? b.b : 0);
+      P Pnx[C];
+      {
+        P bLn[C], FbLn[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          bLn[c] = shfl_down1(bL[c]);
+          FbLn[c] = shfl_down1(FbL[c]);
+        }
+        force_face<D, 0>(bR, FbR, bLn, FbLn, Pnx, qx, nqx, gm1);
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) S_[c] = U[c] - (Pnx[c] - shfl_up1(Pnx[c]));
+      T* x0 = sx + j0 * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        x0[c * W] = S_[c].x;
+        x0[(C + c) * W] = S_[c].y;  // row j1 = j0 + 1 follows row j0 in sx
+      }
+    }
+    __syncthreads();  // (A) stage s consumed; U* published
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      issue(i + 2);
+    }
+    // ---- Y1: evolved y boundary values of both rows (partner row from registers)
+    P byL[C], FbyL[C], byR[C], FbyR[C];
+    {
+      const T* rm = sx + max(j0 - 1, 0) * C * W + lane;      // row 2w-1
+      const T* rp = sx + min(j1 + 1, R - 1) * C * W + lane;  // row 2w+2
+      P Sm[C], Sp[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Sm[c] = P(rm[c * W], S_[c].x);
+        Sp[c] = P(S_[c].y, rp[c * W]);
+      }
+      const PkDom b = hancock<D, 1>(Sm, S_, Sp, h2y, gm1, byL, FbyL, byR, FbyR);
+      const bool xo = lane_out & (xv < SX);
+      bad |= ((xo & y1a & (yr0 >= -1) & (yr0 <= SY)) ? b.a : 0) |
+             ((xo & y1b & (yr1 >= -1) & (yr1 <= SY)) ? b.b : 0);
+      T* w1 = br + warp * 2 * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        w1[c * W] = byR[c].y;
+        w1[(C + c) * W] = FbyR[c].y;
+      }
+    }
+    __syncthreads();  // (B) Ubar^R_y of rows 2w+1 published
+    // ---- Y2: faces (2w-1 | 2w) and (2w | 2w+1)
+    P Py[C];
+    {
+      const T* r = br + wdn * 2 * C * W + lane;
+      P pR[C], pF[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        pR[c] = P(r[c * W], byR[c].x);
+        pF[c] = P(r[(C + c) * W], FbyR[c].x);
+      }
+      force_face<D, 1>(pR, pF, byL, FbyL, Py, qy, nqy, gm1);
+      T* fw = fyb + warp * C * W + lane;
+#pragma unroll
+      for (int c = 0; c < C; ++c) fw[c * W] = Py[c].x;
+    }
+    (void)y2a;
+    (void)y2b;
+    __syncthreads();  // (C) faces below each pair published
+    // ---- update + store
+    if (lane_out & (xv < SX)) {
+      const T* fu = fyb + wup * C * W + lane;  // face below row 2w+2
+      P o[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) o[c] = S_[c] - (P(Py[c].y, fu[c * W]) - P(Py[c].x, Py[c].y));
+      const int64_t cs = g.cstride;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int yr = h ? yr1 : yr0;
+        if (!(h ? upb : upa) || yr >= SY) continue;
+        T v[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[c] = h ? o[c].y : o[c].x;
+        T* dst = a.out + (g.row(yr, zp) * g.rstride + (int)g.xo + xv);
+#pragma unroll
+        for (int c = 0; c < C; ++c) dst[c * cs] = v[c];
+        nan = max(nan, max(naninf(v[0]), naninf(v[C - 1])));
+        if (ws) wmax = fmax(wmax, wavespeed<D>(v, a.gm1, gam));
+        const bool zf = D == 3 && ((zp < g.pad) | (zp >= SZ - g.pad));
+        if ((yr < g.pad) | (yr >= SY - g.pad) | (xv < g.pad) | (xv >= SX - g.pad) | zf)
+          images<D, 0>(a, xv, yr, zp, v);
+      }
+    }
+    win += Gr;
+    yq += Gq;
+    if (win >= nwin) {
+      win -= nwin;
+      ++yq;
+    }
+  }
+  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
+}
+
+template <typename T, int NW, int MB, int D = 2>
+static void launch_o2p(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  using P = typename std::conditional<sizeof(T) == 8, pd, pk>::type;
+  constexpr int W = 32, R = 2 * NW, C = D + 2;
+  using SM = SmemO2<T, R, C>;
+  const size_t bytes = (size_t)(2 * SM::STAGE + R * C * W + NW * 3 * C * W) * sizeof(T) + 64;
+  const int nwin = (int)((a.g.S[0] + (W - 4) - 1) / (W - 4));
+  const int nyb = (int)((a.g.S[1] + (R - 4) - 1) / (R - 4));
+  const int ntiles = nwin * nyb * (D == 3 ? (int)a.g.S[2] : 1);
+  if constexpr (sizeof(T) == 4) pk_set_negzero(s);
+  static int cache[kMaxDevices] = {0};
+  const int per_sm = resident_ctas(k_step2d_o2p<P, D, NW, MB>, 32 * NW, bytes, cache);
+  int grid = per_sm * sm_count();
+  if (grid > ntiles) grid = ntiles;
+  k_step2d_o2p<P, D, NW, MB><<<grid, 32 * NW, bytes, s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb, ntiles);
+}
+
 // order-2 variants (RPL_VARIANT; box rows = NW)
 static int o2_rows(int variant) {
   switch (variant) {
     case 70: return 16;
     case 71: return 12;
     case 72: return 12;
+    case 74: return 24;  // row pairs, 12 warps
+    case 75: return 16;  // row pairs, 8 warps x 2 CTAs
     default: return 24;  // 0 / 73: the default (DESIGN.md tuning log)
   }
 }
@@ -687,6 +898,8 @@ static void launch_step2d_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s
     case 70: return launch_o2<T, 16, 1>(a, tmap, s);
     case 71: return launch_o2<T, 12, 2>(a, tmap, s);
     case 72: return launch_o2<T, 12, 1>(a, tmap, s);
+    case 74: return launch_o2p<T, 12, 1>(a, tmap, s);
+    case 75: return launch_o2p<T, 8, 2>(a, tmap, s);
     default: return launch_o2<T, 24, 1>(a, tmap, s);
   }
 }

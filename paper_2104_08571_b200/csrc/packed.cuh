@@ -92,6 +92,11 @@ __device__ __forceinline__ pk rcp(pk a) { return pk(rcp(a.x), rcp(a.y)); }
 // domain word per lane (scheme.cuh dom_word)
 struct PkDom {
   int a, b;
+  __device__ __forceinline__ PkDom& operator|=(PkDom o) {
+    a |= o.a;
+    b |= o.b;
+    return *this;
+  }
 };
 __device__ __forceinline__ PkDom dom_word(pk rho, pk p) {
   return PkDom{dom_word(rho.x, p.x), dom_word(rho.y, p.y)};
@@ -124,6 +129,10 @@ __device__ __forceinline__ pd shfl_down1(pd v) {
 __device__ __forceinline__ pd shfl_up1(pd v) {
   return pd(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
 }
+
+// componentwise minmod of pairs (scheme.cuh minmod per lane)
+__device__ __forceinline__ pd minmod(pd a, pd b) { return pd(minmod(a.x, b.x), minmod(a.y, b.y)); }
+__device__ __forceinline__ pk minmod(pk a, pk b) { return pk(minmod(a.x, b.x), minmod(a.y, b.y)); }
 
 // element type of a pair type
 template <typename P> struct PairElem;
