@@ -595,3 +595,54 @@ def test_shock_bubble_robustness_oracle():
     # the shock has passed the bubble (centre x = 0.4): the post-shock density 4.46 of
     # the initial state left of x = 0.1 now fills the domain's right half
     assert rho[:, 96:].mean() > 2.0
+
+
+def _force_step_exact(U, lam, gamma, nsteps):
+    """Toro's FORCE scheme (sec. 7.3 / Listing 8, 1-D, transmissive
+    ghosts) written from its textbook definition in exact rational arithmetic:
+      F(U) = [m, m^2/rho + p, (E + p) m/rho],  p = (gamma - 1)(E - m^2 / (2 rho))
+      F_LF  = 1/2 (F_L + F_R) - 1/2 (1/lam) (U_R - U_L)
+      U_RI  = 1/2 (U_L + U_R) - 1/2 lam (F_R - F_L),   F_RI = F(U_RI)
+      F_i+1/2 = 1/2 (F_LF + F_RI);   U_i <- U_i - lam (F_i+1/2 - F_i-1/2)
+    (lam = dt/dx).  No rounding anywhere: FORCE has no square root."""
+    from fractions import Fraction as Fr
+
+    def flux(u):
+        rho, m, E = u
+        p = (gamma - 1) * (E - m * m / (2 * rho))
+        return (m, m * m / rho + p, (E + p) * m / rho)
+
+    half = Fr(1, 2)
+    U = [tuple(Fr(v) for v in cell) for cell in U]
+    for _ in range(nsteps):
+        G = [U[0]] + U + [U[-1]]  # transmissive ghost (clamp)
+        F = [flux(u) for u in G]
+        faces = []
+        for i in range(len(G) - 1):
+            L, R, FL, FR = G[i], G[i + 1], F[i], F[i + 1]
+            flf = tuple(half * (FL[c] + FR[c]) - half / lam * (R[c] - L[c]) for c in range(3))
+            uri = tuple(half * (L[c] + R[c]) - half * lam * (FR[c] - FL[c]) for c in range(3))
+            fri = flux(uri)
+            faces.append(tuple(half * (flf[c] + fri[c]) for c in range(3)))
+        U = [tuple(U[i][c] - lam * (faces[i + 1][c] - faces[i][c]) for c in range(3))
+             for i in range(len(U))]
+    return U
+
+
+def test_exact_rational_steps():
+    """3 FORCE steps on 8 random cells in exact rationals (gamma and
+    dt/dx taken as the exact binary values of their doubles) vs the fp64 oracle:
+    the oracle's result is the exact scheme output up to rounding (<= 1e-13 relative)."""
+    from fractions import Fraction as Fr
+    n = 8
+    U0 = W.random_state((n,), seed=11)
+    dx = 1.0 / n
+    dt = 0.3 * dx / 2.5
+    Uo = oracle.step(oracle.Grid((n,), pad=2, dx=[dx]), U0, dt, 3)
+    lam = Fr(dt) / Fr(dx)
+    Ue = _force_step_exact([tuple(float(v) for v in U0[i]) for i in range(n)], lam,
+                           Fr(1.4), 3)
+    exact = np.array([[float(v) for v in cell] for cell in Ue])
+    scale = np.max(np.abs(exact), axis=0)
+    err = np.max(np.abs(Uo - exact), axis=0) / scale
+    assert np.all(err <= 1e-13), err
