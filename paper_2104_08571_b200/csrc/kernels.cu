@@ -1013,6 +1013,8 @@ int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
     case 38: nw = 10; break;
     case 44: case 45: case 64: nw = 24; break;
     case 63: case 65: case 66: nw = 12; break;
+    case 67: nw = 16; break;
+    case 68: nw = 32; break;
     case 46: nw = 14; break;
     case 47: nw = 20; break;
     default: nw = 12; break;  // 0, 37, 39
@@ -1351,16 +1353,14 @@ static void launch_ra2d(const KArgs<typename PairElem<P>::T>& a, const void* tma
              *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
 }
 
-// Default 2-D order-1 kernel: adjacent row pairs (k_step2d_ra).  12-row tiles of
-// 6 warps, 4 CTAs/SM (variant 66) at small partitions, where the finer granularity
-// shortens the last wave (1024^2: 27.1 us vs 29.1 us for k_step2d_pt); 24-row
-// tiles of 12 warps, 1 CTA/SM, 3-stage ring (variant 64: 22 of 24 rows are
-// outputs) once a partition has >= 32 such tiles per SM (6400x4000: 414 us vs
-// 451 us for k_step2d_pt variant 45; profiles/r1/tile_shape_2d.txt,
-// profiles/r1/ra2d_variants.txt).
+// Default 2-D order-1 kernel: adjacent row pairs (k_step2d_ra), 16-row tiles of 8
+// warps, 3 CTAs/SM (variant 67) at every partition size measured: 1024^2 26.9 us
+// (66: 12-row tiles x 4 CTAs 27.2 us; k_step2d_pt 29.1 us); 6400x4000 396 us (64:
+// 24-row tiles x 1 CTA 415 us; 68: 32-row tiles 404 us; k_step2d_pt variant 45 451
+// us) -- profiles/r1/tile_shape_2d.txt, ra2d_variants.txt.
 int auto_variant_2d(const Geom& g) {
-  const int64_t tiles24 = ((g.S[0] + 29) / 30) * ((g.S[1] + 21) / 22);
-  return tiles24 >= 32LL * sm_count() ? 64 : 66;
+  (void)g;
+  return 67;
 }
 
 template <typename T>
@@ -1387,6 +1387,8 @@ void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     case 64: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 12, 1, 3>(a, tmap, s);
     case 65: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 6, 3, 2>(a, tmap, s);
     case 66: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 6, 4, 2>(a, tmap, s);
+    case 67: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 8, 3, 2>(a, tmap, s);
+    case 68: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 16, 1, 3>(a, tmap, s);
     default: return launch_pt2d<T, 1, 12, 2>(a, tmap, s);  // 0 / 37: the default
   }
 }

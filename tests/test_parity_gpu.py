@@ -369,7 +369,7 @@ def test_flux_difference_tiled_equals_plain_bitwise(dtype, n, pad, parts):
 
 
 @pytest.mark.parametrize("variant", ["31", "34", "37", "44", "45", "46", "48", "49", "63", "64",
-                                     "65", "66"])
+                                     "65", "66", "67", "68"])
 @pytest.mark.parametrize("parts", [(1, 1), (2, 3)])
 def test_2d_kernel_variants_bitwise(variant, parts, monkeypatch):
     """Every 2-D fused kernel variant (RPL_VARIANT, DESIGN.md tuning log) gives
