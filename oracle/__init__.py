@@ -45,7 +45,7 @@ def build(force: bool = False) -> str:
         os.path.getmtime(p) > os.path.getmtime(_LIB_PATH) for p in _DEPS)
     if stale:
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
-        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-std=c11",
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-std=c11",
                "-o", tmp] + _SRC + ["-lm"]
         subprocess.check_call(cmd)
         os.replace(tmp, _LIB_PATH)
@@ -83,6 +83,9 @@ def _L():
         _lib.orc_flux_difference_f64.argtypes = [gp, dp, ctypes.c_double, dp]
         _lib.orc_flux_difference_f32.argtypes = [gp, fp, ctypes.c_double, fp]
         _lib.orc_riemann_exact.argtypes = [ctypes.c_double] * 7 + [dp, ctypes.c_long, dp, dp]
+        _lib.orc_set_threads.argtypes = [ctypes.c_int]
+        _lib.orc_set_threads.restype = ctypes.c_int
+        _lib.orc_set_threads(1)  # single-threaded unless set_threads() asks for more
     return _lib
 
 
@@ -125,6 +128,12 @@ class Grid:
 
 class DomainError(RuntimeError):
     pass
+
+
+def set_threads(n: int) -> int:
+    """OpenMP threads of the oracle's line loops (step, sweep, flux_difference);
+    default 1.  Lines are independent: results are bitwise the same for any count."""
+    return int(_L().orc_set_threads(int(n)))
 
 
 def _check(rc):

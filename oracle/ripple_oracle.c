@@ -5,7 +5,7 @@
  * bench.py cpu_baseline / --impl reference legs, never by the product path.
  * Shares no code with paper_2104_08571_b200/ or include/.
  *
- * Build: gcc -O2 -ffp-contract=off -fPIC -shared (see oracle/build.py).
+ * Build: gcc -O2 -ffp-contract=off -fopenmp -fPIC -shared (oracle/__init__.py build()).
  * -ffp-contract=off keeps every a*b+c as two rounded operations, exactly as
  * written below (reading S21).
  *
@@ -15,6 +15,21 @@
 
 #include <math.h>
 #include <stdlib.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* Threads of the line loops (OpenMP; 1 unless set).  The bench's cpu_baseline times
+ * the oracle at 1 thread and at all host cores; results are identical either way. */
+int orc_set_threads(int n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n < 1 ? 1 : n);
+  return n < 1 ? 1 : n;
+#else
+  (void)n;
+  return 1;
+#endif
+}
 
 #define REAL double
 #define SFX f64

@@ -86,6 +86,11 @@ int orc_riemann_exact(double rl, double ul, double pl, double rr, double ur,
                       double pr, double gamma, const double* xi, long nxi,
                       double* star, double* out);
 
+/* OpenMP threads of the line loops of step/sweep/flux_difference (default 1).
+ * Lines are independent, so results are bitwise the same for any count.
+ * Returns the count set (1 when built without OpenMP). */
+int orc_set_threads(int n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <limits.h>
 #include <stdlib.h>
+
+#include <type_traits>
 
 #include "async.cuh"
 #include "launch.cuh"
@@ -732,6 +735,506 @@ __global__ void __launch_bounds__(32 * NW, MB)
   if (ws) publish_max(a, wmax);
 }
 
+// ------------------------------------------------------------------------
+// k_step3d_rb: the k_step3d_ra tile walk (adjacent row pairs, TMA ring, two CTA
+// barriers per plane) with the per-plane bookkeeping taken off the issue path
+// (round-2 ncu: 61 % of k_step3d_ra's issued instructions were not arithmetic,
+// and IMAD moves compete with FFMA2 for the FMA pipe):
+//  * domain check: per row of the pair one running minimum of hi(rho),
+//    hi(p) over the states the sweeps read -- U^n (x-flux), U* (y-flux), U** (z-flux)
+//    -- and one running maximum of the outputs' |bits| (NaN/Inf), unmasked in the
+//    loop (one VIMNMX3 per state); the lane's loop-invariant output mask is applied
+//    once after the march.  Checking exactly the tile's output cells covers every
+//    interior cell once (the ghost and halo cells other tiles' lanes hold are copies
+//    of interior cells, checked by their owners);
+//  * the z-march state (U**, F_z of the previous plane, the last z-face) ping-pongs
+//    between two register sets (plane loop unrolled by two): nothing is copied;
+//  * ghost images behind a CTA-uniform test (tile within pad of a partition face in
+//    x or y, or a boundary plane); stores predicated;
+//  * NS-stage TMA ring (loads issued NS planes ahead).
+// Per cell and face the operations are scheme.cuh's, in the same order: bitwise
+// equal to k_step3d_ra / k_step3d / k_sweep.
+// ------------------------------------------------------------------------
+template <int NW, typename T, int NS>
+struct SmemRB {
+  static constexpr int W = 32, R = 2 * NW, C = 5;
+  static constexpr int AL = 16 / (int)sizeof(T);
+  static constexpr int WB = W + AL;
+  static constexpr int STAGE = R * C * WB;
+  static constexpr int XY = NW * 2 * C * W;  // (U*, F_y) of row 2w+1, per warp
+  static constexpr int FY = NW * C * W;      // face below row 2w, per warp
+  static constexpr size_t bytes() { return (size_t)(NS * STAGE + XY + FY) * sizeof(T) + 8 * NS; }
+};
+
+template <typename P>
+struct ZPlane {
+  P us[5];  // U** of the previous plane
+  P fz[5];  // F_z(U**) of the previous plane
+  P ph[5];  // z-face below the previous plane
+};
+
+template <int NW, int MB, int L, typename P, int NS, bool UZ>
+__global__ void __launch_bounds__(32 * NW, MB)
+    k_step3d_rb(const __grid_constant__ KArgs<typename PairElem<P>::T> a,
+                const __grid_constant__ CUtensorMap tmap, int nwin, int nyb) {
+  using T = typename PairElem<P>::T;
+  constexpr int D = 3, C = 5, W = 32, R = 2 * NW, TY = R - 2;
+  using SM = SmemRB<NW, T, NS>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  T* stage = reinterpret_cast<T*>(smem);
+  T* xy = stage + NS * SM::STAGE;
+  T* fyb = xy + SM::XY;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + SM::FY);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int t = blockIdx.x;
+  const int win = t % nwin;
+  t /= nwin;
+  const int yb = t % nyb;
+  const int zc = t / nyb;
+  const int xw = win * (W - 2) - 1;
+  const int y0 = yb * TY;
+  const int z0 = zc * a.rows;
+  const int z1 = min(z0 + a.rows, (int)g.S[2]);
+  const int SX = (int)g.S[0], SY = (int)g.S[1], SZ = (int)g.S[2], pad = g.pad;
+  const int j0 = 2 * warp, j1 = 2 * warp + 1;
+  const int yr0 = y0 - 1 + j0, yr1 = y0 - 1 + j1;
+  const int xs = xw + lane;
+  // CTA-uniform: some output cell of the tile lies within pad of an x or y partition face
+  const bool edge_xy = (xw + 1 < pad) | (xw + W - 2 >= SX - pad) | (y0 < pad) |
+                       (y0 + TY - 1 >= SY - pad);
+  Coef<T> kc;
+  if (!step_coef(a, kc)) return;
+  const bool ws = a.cf.dev != nullptr;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int sh = (int)(g.xo + xw) % SM::AL;
+  const int tx = (int)(g.xo + xw) - sh, ty = (int)(g.off[1] + y0 - 1);
+  const int nplanes = z1 - (z0 - 1) + 1;
+  auto issue = [&](int kz) {
+    if (kz >= nplanes) return;
+    const int s = kz % NS;
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
+    tma_load_4d(stage + s * SM::STAGE, &tmap, &bar[s], L == 0 ? tx : tx * C, 0, ty,
+                (int)(g.off[2] + z0 - 1 + kz));
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) issue(s);
+  }
+
+  // domain minima (U^n, U*, U**) and output NaN/Inf maxima, per row of the pair
+  int dm0 = INT_MAX, dm1 = INT_MAX, nn0 = 0, nn1 = 0;
+  T wmax = T(0);
+  const P gm1(a.gm1);
+  const P qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]), nqy(kc.nq2[1]), qz(kc.q[2]), nqz(kc.nq2[2]);
+  const int64_t plane = g.rstride * g.P[1], cs = g.cstride;
+  T* dst0 = a.out + g.row(yr0, z0 - 1) * g.rstride + (g.xo + xs) * g.xstride;
+  T* dst1 = dst0 + g.rstride;
+  const int wdn = max(warp - 1, 0), wup = min(warp + 1, NW - 1);
+  // stage reads of this lane's two rows
+  constexpr int cst = L == 0 ? SM::WB : 1;
+  const int xoff = (L == 0 ? sh + lane : (sh + lane) * C) + j0 * C * SM::WB;
+  // per-lane output masks (loop-invariant)
+  const bool out_x = (lane >= 1) & (lane <= W - 2) & (xs < SX);
+  const bool st0 = out_x & (j0 >= 1) & (yr0 < SY);
+  const bool st1 = out_x & (j1 <= TY) & (yr1 < SY);
+
+  auto body = [&](const int kz, const ZPlane<P>& zp, ZPlane<P>& zn) {
+    const int s = kz % NS;
+    mbar_wait(&bar[s], (kz / NS) & 1);
+    P U[C], F[C], S_[C], G[C];
+    {
+      const T* r0 = stage + s * SM::STAGE + xoff;
+      const T* r1 = r0 + C * SM::WB;
+#pragma unroll
+      for (int c = 0; c < C; ++c) U[c] = P(r0[c * cst], r1[c * cst]);
+    }
+    dom_min(dm0, dm1, U[0], flux_p<D, 0>(U, F, gm1));
+    {
+      P Un[C], Fn[C], Pnx[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        Un[c] = shfl_down1(U[c]);
+        Fn[c] = shfl_down1(F[c]);
+      }
+      force_face<D, 0>(U, F, Un, Fn, Pnx, qx, nqx, gm1);
+#pragma unroll
+      for (int c = 0; c < C; ++c) S_[c] = U[c] - (Pnx[c] - shfl_up1(Pnx[c]));
+    }
+    dom_min(dm0, dm1, S_[0], flux_p<D, 1>(S_, G, gm1));
+    {
+      T* x1 = xy + warp * 2 * C * W + lane;  // row 2w+1 for warp w+1
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        x1[c * W] = S_[c].y;
+        x1[(C + c) * W] = G[c].y;
+      }
+    }
+    __syncthreads();  // (A) stage s consumed, rows 2w+1 published
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      issue(kz + NS);
+    }
+    // Y: faces (2w-1 | 2w) and (2w | 2w+1) in one pair evaluation
+    P Py[C];
+    {
+      const T* pdn = xy + wdn * 2 * C * W + lane;
+      P SL[C], GL[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        SL[c] = P(pdn[c * W], S_[c].x);
+        GL[c] = P(pdn[(C + c) * W], G[c].x);
+      }
+      force_face<D, 1>(SL, GL, S_, G, Py, qy, nqy, gm1);
+      T* f0 = fyb + warp * C * W + lane;  // face below row 2w, for warp w-1
+#pragma unroll
+      for (int c = 0; c < C; ++c) f0[c * W] = Py[c].x;
+    }
+    __syncthreads();  // (B) faces published
+    {
+      const T* fu = fyb + wup * C * W + lane;  // face below row 2w+2 (warp w+1)
+#pragma unroll
+      for (int c = 0; c < C; ++c) zn.us[c] = S_[c] - (P(Py[c].y, fu[c * W]) - Py[c]);
+      dom_min(dm0, dm1, zn.us[0], flux_p<D, 2>(zn.us, zn.fz, gm1));
+      if (kz >= 1) {
+        force_face<D, 2>(zp.us, zp.fz, zn.us, zn.fz, zn.ph, qz, nqz, gm1);
+        if (kz >= 2) {
+          // update and store plane z - 1
+          P o[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) o[c] = zp.us[c] - (zn.ph[c] - zp.ph[c]);
+          dst0 += plane;
+          dst1 += plane;
+          nn0 = max(nn0, max(naninf(o[0].x), naninf(o[C - 1].x)));
+          nn1 = max(nn1, max(naninf(o[0].y), naninf(o[C - 1].y)));
+          if (st0) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) dst0[c * cs] = o[c].x;
+          }
+          if (st1) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) dst1[c * cs] = o[c].y;
+          }
+          if (ws) {
+            T v0[C], v1[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+              v0[c] = o[c].x;
+              v1[c] = o[c].y;
+            }
+            const T gam = (T)a.cf.gamma;
+            if (st0) wmax = fmax(wmax, wavespeed<D>(v0, a.gm1, gam));
+            if (st1) wmax = fmax(wmax, wavespeed<D>(v1, a.gm1, gam));
+          }
+          const int zo = z0 - 2 + kz;  // the stored plane
+          const bool zf = (zo < pad) | (zo >= SZ - pad);
+          if (edge_xy | zf) {
+            const bool xface = (xs < pad) | (xs >= SX - pad);
+            const bool yf0 = (yr0 < pad) | (yr0 >= SY - pad);
+            const bool yf1 = (yr1 < pad) | (yr1 >= SY - pad);
+            if (st0 & (xface | yf0 | zf)) {
+              T v[C];
+#pragma unroll
+              for (int c = 0; c < C; ++c) v[c] = o[c].x;
+              if (g.img_fast)
+                images_single<D>(g, a.out, xs, yr0, zo, v);
+              else
+                images3_nl<D, L, T>(&a, xs, yr0, zo, v[0], v[1], v[2], v[3], v[4]);
+            }
+            if (st1 & (xface | yf1 | zf)) {
+              T v[C];
+#pragma unroll
+              for (int c = 0; c < C; ++c) v[c] = o[c].y;
+              if (g.img_fast)
+                images_single<D>(g, a.out, xs, yr1, zo, v);
+              else
+                images3_nl<D, L, T>(&a, xs, yr1, zo, v[0], v[1], v[2], v[3], v[4]);
+            }
+          }
+        }
+      }
+    }
+  };
+
+  ZPlane<P> za, zb;
+  int kz = 0;
+  if constexpr (UZ) {
+    for (; kz + 2 <= nplanes; kz += 2) {
+      body(kz, za, zb);
+      body(kz + 1, zb, za);
+    }
+    if (kz < nplanes) body(kz, za, zb);
+  } else {
+#pragma unroll 1
+    for (; kz < nplanes; ++kz) {
+      body(kz, za, zb);
+      za = zb;
+    }
+  }
+
+  // the output masks, applied once
+  const bool bad = (st0 & ((dm0 <= 0) | (nn0 >= kExpMask<T>))) |
+                   (st1 & ((dm1 <= 0) | (nn1 >= kExpMask<T>)));
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
+}
+
+// ------------------------------------------------------------------------
+// k_step3d_sp: k_step3d_rb software-pipelined across planes.  After barrier (B) of
+// plane k a warp waits for stage k+1 and then runs, in one basic block, the
+// x-sweep of plane k+1 and the y-update + z-march of plane k -- two independent
+// instruction streams the scheduler interleaves (ncu on k_step3d_rb: the z-march
+// region stalled on fixed-latency dependencies while the FMA pipe idled).  Row
+// 2w+1 of plane k+1 is published after (B) of plane k, when every warp is done
+// reading plane k's rows.  Stores are predicated (no branch splits the block);
+// ghost images and the device-CFL wavespeed follow it behind uniform branches.
+// Same per-cell operations as k_step3d_rb (bitwise equal).
+// ------------------------------------------------------------------------
+__device__ __forceinline__ void st_if(float* p, float v, bool ok) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f32 [%0], %1;\n}" ::"l"(p),
+               "f"(v), "r"((int)ok)
+               : "memory");
+}
+__device__ __forceinline__ void st_if(double* p, double v, bool ok) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f64 [%0], %1;\n}" ::"l"(p),
+               "d"(v), "r"((int)ok)
+               : "memory");
+}
+
+template <int NW, int MB, int L, typename P, int NS>
+__global__ void __launch_bounds__(32 * NW, MB)
+    k_step3d_sp(const __grid_constant__ KArgs<typename PairElem<P>::T> a,
+                const __grid_constant__ CUtensorMap tmap, int nwin, int nyb) {
+  using T = typename PairElem<P>::T;
+  constexpr int D = 3, C = 5, W = 32, R = 2 * NW, TY = R - 2;
+  using SM = SmemRB<NW, T, NS>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  T* stage = reinterpret_cast<T*>(smem);
+  T* xy = stage + NS * SM::STAGE;
+  T* fyb = xy + SM::XY;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + SM::FY);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int t = blockIdx.x;
+  const int win = t % nwin;
+  t /= nwin;
+  const int yb = t % nyb;
+  const int zc = t / nyb;
+  const int xw = win * (W - 2) - 1;
+  const int y0 = yb * TY;
+  const int z0 = zc * a.rows;
+  const int z1 = min(z0 + a.rows, (int)g.S[2]);
+  const int SX = (int)g.S[0], SY = (int)g.S[1], SZ = (int)g.S[2], pad = g.pad;
+  const int j0 = 2 * warp, j1 = 2 * warp + 1;
+  const int yr0 = y0 - 1 + j0, yr1 = y0 - 1 + j1;
+  const int xs = xw + lane;
+  const bool edge_xy = (xw + 1 < pad) | (xw + W - 2 >= SX - pad) | (y0 < pad) |
+                       (y0 + TY - 1 >= SY - pad);
+  Coef<T> kc;
+  if (!step_coef(a, kc)) return;
+  const bool ws = a.cf.dev != nullptr;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int sh = (int)(g.xo + xw) % SM::AL;
+  const int tx = (int)(g.xo + xw) - sh, ty = (int)(g.off[1] + y0 - 1);
+  const int nplanes = z1 - (z0 - 1) + 1;  // >= 3
+  auto issue = [&](int kz) {
+    if (kz >= nplanes) return;
+    const int s = kz % NS;
+    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
+    tma_load_4d(stage + s * SM::STAGE, &tmap, &bar[s], L == 0 ? tx : tx * C, 0, ty,
+                (int)(g.off[2] + z0 - 1 + kz));
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) issue(s);
+  }
+
+  int dm0 = INT_MAX, dm1 = INT_MAX, nn0 = 0, nn1 = 0;
+  T wmax = T(0);
+  const P gm1(a.gm1);
+  const P qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]), nqy(kc.nq2[1]), qz(kc.q[2]), nqz(kc.nq2[2]);
+  const int64_t plane = g.rstride * g.P[1], cs = g.cstride;
+  T* dst0 = a.out + g.row(yr0, z0 - 1) * g.rstride + (g.xo + xs) * g.xstride;
+  T* dst1 = dst0 + g.rstride;
+  const int wdn = max(warp - 1, 0), wup = min(warp + 1, NW - 1);
+  constexpr int cst = L == 0 ? SM::WB : 1;
+  const int xoff = (L == 0 ? sh + lane : (sh + lane) * C) + j0 * C * SM::WB;
+  const bool out_x = (lane >= 1) & (lane <= W - 2) & (xs < SX);
+  const bool st0 = out_x & (j0 >= 1) & (yr0 < SY);
+  const bool st1 = out_x & (j1 <= TY) & (yr1 < SY);
+  T* const x1 = xy + warp * 2 * C * W + lane;   // row 2w+1 for warp w+1
+  const T* const pdn = xy + wdn * 2 * C * W + lane;
+  T* const f0 = fyb + warp * C * W + lane;      // face below row 2w, for warp w-1
+  const T* const fu = fyb + wup * C * W + lane;  // face below row 2w+2 (warp w+1)
+
+  // X: stage of plane kz -> (U*, F_y(U*)) of rows 2w, 2w+1
+  auto xphase = [&](const int kz, P* S_, P* G) {
+    const int s = kz % NS;
+    mbar_wait(&bar[s], (kz / NS) & 1);
+    P U[C], F[C];
+    const T* r0 = stage + s * SM::STAGE + xoff;
+    const T* r1 = r0 + C * SM::WB;
+#pragma unroll
+    for (int c = 0; c < C; ++c) U[c] = P(r0[c * cst], r1[c * cst]);
+    dom_min(dm0, dm1, U[0], flux_p<D, 0>(U, F, gm1));
+    P Un[C], Fn[C], Pnx[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      Un[c] = shfl_down1(U[c]);
+      Fn[c] = shfl_down1(F[c]);
+    }
+    force_face<D, 0>(U, F, Un, Fn, Pnx, qx, nqx, gm1);
+#pragma unroll
+    for (int c = 0; c < C; ++c) S_[c] = U[c] - (Pnx[c] - shfl_up1(Pnx[c]));
+    dom_min(dm0, dm1, S_[0], flux_p<D, 1>(S_, G, gm1));
+  };
+  auto publish = [&](const P* S_, const P* G) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      x1[c * W] = S_[c].y;
+      x1[(C + c) * W] = G[c].y;
+    }
+  };
+  // A, TMA refill, Y faces, B
+  auto yphase = [&](const int kz, const P* S_, const P* G, P* Py) {
+    __syncthreads();  // (A) stage kz consumed, rows 2w+1 of plane kz published
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      issue(kz + NS);
+    }
+    P SL[C], GL[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      SL[c] = P(pdn[c * W], S_[c].x);
+      GL[c] = P(pdn[(C + c) * W], G[c].x);
+    }
+    force_face<D, 1>(SL, GL, S_, G, Py, qy, nqy, gm1);
+#pragma unroll
+    for (int c = 0; c < C; ++c) f0[c * W] = Py[c].x;
+    __syncthreads();  // (B) faces published; every warp is done reading plane kz's rows
+  };
+  // y-update + z-march of plane kz: output o of plane kz-1 (kz >= 2), predicated stores
+  // (M: 0 = first plane of the march, 1 = second, 2 = steady state -- compile-time, so
+  // the steady-state block has no branch)
+  auto zphase = [&](auto M, const P* S_, const P* Py, const ZPlane<P>& zp, ZPlane<P>& zn, P* o) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) zn.us[c] = S_[c] - (P(Py[c].y, fu[c * W]) - Py[c]);
+    dom_min(dm0, dm1, zn.us[0], flux_p<D, 2>(zn.us, zn.fz, gm1));
+    constexpr int m = decltype(M)::value;
+    if constexpr (m >= 1) {
+      force_face<D, 2>(zp.us, zp.fz, zn.us, zn.fz, zn.ph, qz, nqz, gm1);
+      if constexpr (m >= 2) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) o[c] = zp.us[c] - (zn.ph[c] - zp.ph[c]);
+        dst0 += plane;
+        dst1 += plane;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          st_if(dst0 + c * cs, o[c].x, st0);
+          st_if(dst1 + c * cs, o[c].y, st1);
+        }
+        nn0 = max(nn0, max(naninf(o[0].x), naninf(o[C - 1].x)));
+        nn1 = max(nn1, max(naninf(o[0].y), naninf(o[C - 1].y)));
+      }
+    }
+  };
+  // ghost images and wavespeed of the stored plane (uniform branches)
+  auto tail = [&](auto M, const int kz, const P* o) {
+    constexpr int m = decltype(M)::value;
+    if constexpr (m < 2) return;
+    if (ws) {
+      T v0[C], v1[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        v0[c] = o[c].x;
+        v1[c] = o[c].y;
+      }
+      const T gam = (T)a.cf.gamma;
+      if (st0) wmax = fmax(wmax, wavespeed<D>(v0, a.gm1, gam));
+      if (st1) wmax = fmax(wmax, wavespeed<D>(v1, a.gm1, gam));
+    }
+    const int zo = z0 - 2 + kz;
+    const bool zf = (zo < pad) | (zo >= SZ - pad);
+    if (edge_xy | zf) {
+      const bool xface = (xs < pad) | (xs >= SX - pad);
+      const bool yf0 = (yr0 < pad) | (yr0 >= SY - pad);
+      const bool yf1 = (yr1 < pad) | (yr1 >= SY - pad);
+      if (st0 & (xface | yf0 | zf)) {
+        T v[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[c] = o[c].x;
+        if (g.img_fast)
+          images_single<D>(g, a.out, xs, yr0, zo, v);
+        else
+          images3_nl<D, L, T>(&a, xs, yr0, zo, v[0], v[1], v[2], v[3], v[4]);
+      }
+      if (st1 & (xface | yf1 | zf)) {
+        T v[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[c] = o[c].y;
+        if (g.img_fast)
+          images_single<D>(g, a.out, xs, yr1, zo, v);
+        else
+          images3_nl<D, L, T>(&a, xs, yr1, zo, v[0], v[1], v[2], v[3], v[4]);
+      }
+    }
+  };
+  // one plane with the next plane's x-sweep overlapped: (Sa, Ga) -> (Sb, Gb)
+  auto full = [&](auto M, const int kz, const P* Sa, const P* Ga, P* Sb, P* Gb,
+                  const ZPlane<P>& zp, ZPlane<P>& zn) {
+    P Py[C], o[C];
+    yphase(kz, Sa, Ga, Py);
+    xphase(kz + 1, Sb, Gb);
+    zphase(M, Sa, Py, zp, zn, o);
+    publish(Sb, Gb);
+    tail(M, kz, o);
+  };
+  auto last = [&](const int kz, const P* Sa, const P* Ga, const ZPlane<P>& zp, ZPlane<P>& zn) {
+    P Py[C], o[C];
+    yphase(kz, Sa, Ga, Py);
+    zphase(std::integral_constant<int, 2>(), Sa, Py, zp, zn, o);
+    tail(std::integral_constant<int, 2>(), kz, o);
+  };
+  using M0 = std::integral_constant<int, 0>;
+  using M1 = std::integral_constant<int, 1>;
+  using M2 = std::integral_constant<int, 2>;
+
+  P SA[C], GA[C], SB[C], GB[C];
+  ZPlane<P> za, zb;
+  xphase(0, SA, GA);
+  publish(SA, GA);
+  full(M0(), 0, SA, GA, SB, GB, za, zb);  // nplanes >= 3
+  full(M1(), 1, SB, GB, SA, GA, zb, za);
+  int kz = 2;
+  for (; kz + 2 < nplanes; kz += 2) {
+    full(M2(), kz, SA, GA, SB, GB, za, zb);
+    full(M2(), kz + 1, SB, GB, SA, GA, zb, za);
+  }
+  if (kz + 1 < nplanes) {
+    full(M2(), kz, SA, GA, SB, GB, za, zb);
+    last(kz + 1, SB, GB, zb, za);
+  } else {
+    last(kz, SA, GA, za, zb);
+  }
+
+  const bool bad = (st0 & ((dm0 <= 0) | (nn0 >= kExpMask<T>))) |
+                   (st1 & ((dm1 <= 0) | (nn1 >= kExpMask<T>)));
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 1u);
+  if (ws) publish_max(a, wmax);
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -772,7 +1275,8 @@ static EncodeTiledFn encode_fn() {
 // w+8: 1111 us); 70: k_step3d_rp with 16 warps / 30 rows, one CTA per SM (slower
 // still, SoA only).  AoS (configs[4] layout comparison) runs the 8-warp forms.
 static bool use_rp(const Geom& g, int variant) {
-  return g.elem == 4 && (variant == 0 || variant == 78 || (variant == 70 && g.layout == 0));
+  return g.elem == 4 && (variant == 0 || variant == 80 || variant == 78 ||
+                         (variant == 70 && g.layout == 0));
 }
 static int rp_warps(int variant) { return variant == 70 ? 16 : 8; }
 
@@ -780,6 +1284,8 @@ static int rp_warps(int variant) { return variant == 70 ? 16 : 8; }
 // fp32 packed: 2 NW - 2 output rows, the box holds 2 NW rows incl. the y-halo)
 static int ty3(const Geom& g, int variant) {
   if (use_rp(g, variant)) return 2 * rp_warps(variant) - 2;
+  if (variant == 98) return 22;
+  if (variant == 99) return 30;
   return variant == 50 ? 30 : (variant == 51 ? 22 : 14);
 }
 
@@ -802,6 +1308,42 @@ static int launch3_ra(const KArgs<typename PairElem<P>::T>& a, const void* tmap,
   static int cache[kMaxDevices] = {0};
   resident_ctas(k_step3d_ra<NW, MB, L, P>, 32 * NW, sm, cache);
   k_step3d_ra<NW, MB, L, P><<<nwin * nyb * nzc, 32 * NW, sm, s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb);
+  return 0;
+}
+
+template <int NW, int MB, int L, typename P, int NS, bool UZ = false>
+static int launch3_rb(const KArgs<typename PairElem<P>::T>& a, const void* tmap,
+                      cudaStream_t s) {
+  using T = typename PairElem<P>::T;
+  constexpr int W = 32, TY = 2 * NW - 2;
+  const Geom& g = a.g;
+  const int nwin = (int)((g.S[0] + (W - 2) - 1) / (W - 2));
+  const int nyb = (int)((g.S[1] + TY - 1) / TY);
+  const int nzc = (int)((g.S[2] + a.rows - 1) / a.rows);
+  const size_t sm = SmemRB<NW, T, NS>::bytes();
+  if constexpr (sizeof(T) == 4) pk_set_negzero(s);
+  static int cache[kMaxDevices] = {0};
+  resident_ctas(k_step3d_rb<NW, MB, L, P, NS, UZ>, 32 * NW, sm, cache);
+  k_step3d_rb<NW, MB, L, P, NS, UZ><<<nwin * nyb * nzc, 32 * NW, sm, s>>>(
+      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb);
+  return 0;
+}
+
+template <int NW, int MB, int L, typename P, int NS>
+static int launch3_sp(const KArgs<typename PairElem<P>::T>& a, const void* tmap,
+                      cudaStream_t s) {
+  using T = typename PairElem<P>::T;
+  constexpr int W = 32, TY = 2 * NW - 2;
+  const Geom& g = a.g;
+  const int nwin = (int)((g.S[0] + (W - 2) - 1) / (W - 2));
+  const int nyb = (int)((g.S[1] + TY - 1) / TY);
+  const int nzc = (int)((g.S[2] + a.rows - 1) / a.rows);
+  const size_t sm = SmemRB<NW, T, NS>::bytes();
+  if constexpr (sizeof(T) == 4) pk_set_negzero(s);
+  static int cache[kMaxDevices] = {0};
+  resident_ctas(k_step3d_sp<NW, MB, L, P, NS>, 32 * NW, sm, cache);
+  k_step3d_sp<NW, MB, L, P, NS><<<nwin * nyb * nzc, 32 * NW, sm, s>>>(
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb);
   return 0;
 }
@@ -858,6 +1400,46 @@ static int launch3(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
 
 template <typename T>
 int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
+  if (a.variant == 0) {
+    // defaults (round 2, profiles/r2/): fp64 k_step3d_sp (software-pipelined planes,
+    // 8 warps, 1 CTA/SM, 3-stage ring): 512^3 4.34 -> 3.90 ms; fp32 k_step3d_rb
+    // (8 warps, 2 CTAs/SM, 3-stage ring): 384^3 1.06 -> 0.99 ms
+    const bool aos = a.g.layout == 1;
+    if constexpr (sizeof(T) == 8)
+      return aos ? launch3_sp<8, 1, 1, pd, 3>(a, tmap, s) : launch3_sp<8, 1, 0, pd, 3>(a, tmap, s);
+    else
+      return aos ? launch3_rb<8, 2, 1, pk, 3>(a, tmap, s) : launch3_rb<8, 2, 0, pk, 3>(a, tmap, s);
+  }
+  if (a.variant == 99) {
+    using P = typename std::conditional<sizeof(T) == 8, pd, pk>::type;
+    return a.g.layout == 1 ? launch3_rb<16, 1, 1, P, 3>(a, tmap, s) : launch3_rb<16, 1, 0, P, 3>(a, tmap, s);
+  }
+  if (a.variant == 98) {
+    using P = typename std::conditional<sizeof(T) == 8, pd, pk>::type;
+    return a.g.layout == 1 ? launch3_sp<12, 1, 1, P, 3>(a, tmap, s) : launch3_sp<12, 1, 0, P, 3>(a, tmap, s);
+  }
+  if (a.variant >= 95 && a.variant <= 97) {
+    using P = typename std::conditional<sizeof(T) == 8, pd, pk>::type;
+    constexpr int MB = sizeof(T) == 8 ? 1 : 2;
+    const bool aos = a.g.layout == 1;
+    switch (a.variant) {
+      case 96: return aos ? launch3_sp<8, MB, 1, P, 3>(a, tmap, s) : launch3_sp<8, MB, 0, P, 3>(a, tmap, s);
+      case 97: return aos ? launch3_sp<8, 1, 1, P, 3>(a, tmap, s) : launch3_sp<8, 1, 0, P, 3>(a, tmap, s);
+      default: return aos ? launch3_sp<8, MB, 1, P, 2>(a, tmap, s) : launch3_sp<8, MB, 0, P, 2>(a, tmap, s);
+    }
+  }
+  if (a.variant >= 90 && a.variant <= 94) {
+    using P = typename std::conditional<sizeof(T) == 8, pd, pk>::type;
+    constexpr int MB = sizeof(T) == 8 ? 1 : 2;
+    const bool aos = a.g.layout == 1;
+    switch (a.variant) {
+      case 91: return aos ? launch3_rb<8, MB, 1, P, 3>(a, tmap, s) : launch3_rb<8, MB, 0, P, 3>(a, tmap, s);
+      case 92: return aos ? launch3_rb<8, MB, 1, P, 4>(a, tmap, s) : launch3_rb<8, MB, 0, P, 4>(a, tmap, s);
+      case 93: return aos ? launch3_rb<8, MB, 1, P, 2, true>(a, tmap, s) : launch3_rb<8, MB, 0, P, 2, true>(a, tmap, s);
+      case 94: return aos ? launch3_rb<8, MB, 1, P, 4, true>(a, tmap, s) : launch3_rb<8, MB, 0, P, 4, true>(a, tmap, s);
+      default: return aos ? launch3_rb<8, MB, 1, P, 2>(a, tmap, s) : launch3_rb<8, MB, 0, P, 2>(a, tmap, s);
+    }
+  }
   if constexpr (sizeof(T) == 4) {
     // packed row pairs (default) -- must match use_rp() / the TMA box
     if (use_rp(a.g, a.variant)) {
@@ -870,9 +1452,9 @@ int launch_step3d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
     }
   }
   if constexpr (sizeof(T) == 8) {
-    // fp64 default: adjacent row pairs, two scalar rows per lane (k_step3d_ra<pd>, 8
-    // warps, 216 registers, 1 CTA/SM): 512^3 4340 us vs 4533 us for k_step3d (56)
-    if (a.variant == 0)
+    // 80: the round-1 fp64 default, adjacent row pairs of doubles (k_step3d_ra<pd>, 8
+    // warps, 216 registers, 1 CTA/SM): 512^3 4340 us
+    if (a.variant == 80)
       return a.g.layout == 1 ? launch3_ra<8, 1, 1, pd>(a, tmap, s) : launch3_ra<8, 1, 0, pd>(a, tmap, s);
   }
   if (a.g.layout == 1) return launch3<T, 1, 14, 1, 1>(a, tmap, s);  // AoS (configs[4])
@@ -908,7 +1490,7 @@ int make_tmap_aos(const Geom& g, const void* buf, void* map_out, int box_cells, 
 }
 
 int make_tmap3d(const Geom& g, const void* buf, void* map_out, int variant) {
-  if (g.layout == 1) return make_tmap_aos(g, buf, map_out, 32 + 16 / g.elem, 14 + 2);
+  if (g.layout == 1) return make_tmap_aos(g, buf, map_out, 32 + 16 / g.elem, ty3(g, variant) + 2);
   return make_tmap(g, buf, map_out, win3(g, variant) + 16 / g.elem,  // + Smem3::AL
                    ty3(g, variant) + 2);
 }

@@ -86,8 +86,21 @@ __device__ __forceinline__ pk fma(pk a, pk b, pk c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pbits(a)), "l"(pbits(b)), "l"(pbits(c)));
   return punpack(r);
 }
-// 1/x per lane: the scalar MUFU + Newton sequence of scheme.cuh
-__device__ __forceinline__ pk rcp(pk a) { return pk(rcp(a.x), rcp(a.y)); }
+// 1/x per lane: the scalar MUFU + Newton sequence of scheme.cuh, the Newton step as
+// two FFMA2 (per lane the same IEEE fma(r, fma(-x, r, 1), r) as the scalar rcp)
+__device__ __forceinline__ pk rcp(pk a) {
+  float r0, r1;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(a.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(a.y));
+  const pk r(r0, r1);
+  return fma(r, fma(-a, r, pk(1.0f)), r);
+}
+
+// running domain minimum per lane (scheme.cuh dom_min)
+__device__ __forceinline__ void dom_min(int& a0, int& a1, pk rho, pk p) {
+  dom_min(a0, rho.x, p.x);
+  dom_min(a1, rho.y, p.y);
+}
 
 // domain word per lane (scheme.cuh dom_word)
 struct PkDom {
@@ -122,6 +135,10 @@ __device__ __forceinline__ pd fma(pd a, pd b, pd c) {
 __device__ __forceinline__ pd rcp(pd a) { return pd(rcp(a.x), rcp(a.y)); }
 __device__ __forceinline__ PkDom dom_word(pd rho, pd p) {
   return PkDom{dom_word(rho.x, p.x), dom_word(rho.y, p.y)};
+}
+__device__ __forceinline__ void dom_min(int& a0, int& a1, pd rho, pd p) {
+  dom_min(a0, rho.x, p.x);
+  dom_min(a1, rho.y, p.y);
 }
 __device__ __forceinline__ pd shfl_down1(pd v) {
   return pd(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));

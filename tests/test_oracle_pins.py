@@ -646,3 +646,26 @@ def test_exact_rational_steps():
     scale = np.max(np.abs(exact), axis=0)
     err = np.max(np.abs(Uo - exact), axis=0) / scale
     assert np.all(err <= 1e-13), err
+
+
+@pytest.mark.parametrize("n,order", [((37,), 1), ((23, 17), 1), ((11, 9, 7), 1), ((19, 13), 2),
+                                     ((9, 8, 7), 2)])
+def test_oracle_threads_bitwise(n, order):
+    """The oracle's OpenMP line loops (bench cpu_baseline at all host cores) give the
+    single-thread result bit for bit: each line writes only its own cells."""
+    D = len(n)
+    dx = [1.0 / n[0]] * D
+    U0 = W.random_state(n, seed=23)
+    g = oracle.Grid(n, dx=dx, order=order)
+    dt = 0.2 * dx[0] / 3.0
+    try:
+        oracle.set_threads(1)
+        ref = oracle.step(g, U0, dt, 4)
+        fd1 = oracle.flux_difference(oracle.Grid(n, pad=1, dx=dx), U0, dt)
+        for th in (2, 3, 8):
+            oracle.set_threads(th)
+            assert np.array_equal(oracle.step(g, U0, dt, 4).view(np.uint64), ref.view(np.uint64))
+            fd = oracle.flux_difference(oracle.Grid(n, pad=1, dx=dx), U0, dt)
+            assert np.array_equal(fd.view(np.uint64), fd1.view(np.uint64))
+    finally:
+        oracle.set_threads(1)

@@ -491,7 +491,11 @@ def test_full_size_sampled_flux_difference_fd8k():
 
 @pytest.mark.parametrize("variant,dtype", [("0", "f32"), ("20", "f32"), ("21", "f32"),
                                            ("70", "f32"), ("78", "f32"), ("56", "f64"), ("21", "f64"), ("51", "f64"),
-                                           ("51", "f32")])
+                                           ("51", "f32"), ("90", "f32"), ("91", "f32"), ("92", "f32"),
+                                           ("93", "f32"), ("94", "f32"), ("90", "f64"), ("92", "f64"),
+                                           ("93", "f64"), ("94", "f64"), ("95", "f32"), ("96", "f32"),
+                                           ("97", "f32"), ("95", "f64"), ("96", "f64"), ("98", "f32"),
+                                           ("99", "f32"), ("80", "f32"), ("80", "f64")])
 def test_3d_kernel_variants_bitwise(variant, dtype, monkeypatch):
     """3-D fused variants (RPL_VARIANT: 0 = default, for fp32 the packed adjacent
     row-pair kernel (FFMA2, in-register y-face, 8 warps / 14 rows); 78 = packed
