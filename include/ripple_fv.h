@@ -201,6 +201,20 @@ rpl_status rpl_launches_per_step(const rpl_domain* dom, int32_t* out);
 rpl_status rpl_profile(rpl_domain* dom, int32_t max_launches);
 rpl_status rpl_profile_read(rpl_domain* dom, double* kernel_ms, int64_t* launches);
 
+/* Name of the kernel that rpl_advance (op 0) or rpl_flux_difference (op 1) launches
+ * for this domain's configuration (for roofline reports, e.g. "k_step3d_sp<pd>").
+ * Static string, owned by the library; "" for a null domain or an unknown op. */
+const char* rpl_kernel_name(const rpl_domain* dom, int32_t op);
+
+/* Exposed halo time (event-timed: t(halo_ready) - t(interior_done)).
+ * While rpl_profile is enabled on a multi-rank domain, rpl_advance also records an
+ * event pair around every halo exchange: after the step kernels (interior done) and
+ * after the exchange (NCCL pack/send/recv/unpack, or the P2P epoch sync that waits
+ * for the neighbours' halo stores: halo ready).  Synchronises; returns the summed
+ * milliseconds and exchange count since the last read, and resets.  Single-rank
+ * domains have no exchange: 0 ms, 0 exchanges.  Errors: RPL_E_INVALID_ARG (null). */
+rpl_status rpl_profile_halo(rpl_domain* dom, double* halo_ms, int64_t* exchanges);
+
 /* Halo transfer plan (host only, no GPU).  Every ghost cell of every partition
  * has exactly one source interior cell (sequential per-dim fill semantics,
  * S:193); the plan lists, for every (source partition, destination partition)

@@ -47,6 +47,7 @@ EXPORTS = ["rpl_config_init", "rpl_config_check", "rpl_arena_bytes", "rpl_nccl_u
            "rpl_fill_padding", "rpl_advance", "rpl_max_wavespeed", "rpl_advance_cfl",
            "rpl_advance_to",
            "rpl_synchronize", "rpl_launches_per_step", "rpl_profile", "rpl_profile_read",
+           "rpl_profile_halo", "rpl_kernel_name",
            "rpl_halo_plan", "rpl_p2p_export", "rpl_p2p_attach",
            "rpl_flux_difference", "rpl_get_flux_difference", "rpl_destroy",
            "rpl_last_error"]
@@ -87,6 +88,9 @@ def lib():
     L.rpl_launches_per_step.argtypes = [vp, P(ctypes.c_int32)]
     L.rpl_profile.argtypes = [vp, ctypes.c_int32]
     L.rpl_profile_read.argtypes = [vp, P(ctypes.c_double), P(ctypes.c_int64)]
+    L.rpl_profile_halo.argtypes = [vp, P(ctypes.c_double), P(ctypes.c_int64)]
+    L.rpl_kernel_name.argtypes = [vp, ctypes.c_int32]
+    L.rpl_kernel_name.restype = ctypes.c_char_p
     L.rpl_halo_plan.argtypes = [P(Config), P(HaloEdge), ctypes.c_int32, P(ctypes.c_int32)]
     L.rpl_p2p_export.argtypes = [vp, vp, P(ctypes.c_size_t)]
     L.rpl_p2p_attach.argtypes = [vp, vp, ctypes.c_size_t]

@@ -31,17 +31,6 @@ namespace rpl {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-template <typename T>
-struct Vec2;
-template <>
-struct Vec2<double> {
-  using type = double2;
-};
-template <>
-struct Vec2<float> {
-  using type = float2;
-};
-
 template <int D, int L, typename T>
 __device__ __forceinline__ void load_cell(const Geom& g, const T* __restrict__ buf, int64_t x,
                                           int64_t y, int64_t z, T* v) {
@@ -154,24 +143,10 @@ __global__ void __launch_bounds__(256) k_sweep2(const __grid_constant__ KArgs<T>
   if (ws) publish_max(a, wmax);
 }
 
-template <typename T, int V>
-struct VecV;
-template <typename T>
-struct VecV<T, 1> {
-  using type = T;
-};
-template <typename T>
-struct VecV<T, 2> {
-  using type = typename Vec2<T>::type;
-};
+constexpr int kRows2 = 16;  // 2-D order-1 tile rows (box), 14 outputs
 
-// ---------------------------------------------------------------------------
-// K-B (2-D), persistent TMA form (the default).  A tile is one x-window (32V
-// slots, 32V-2 outputs) x NW rows; each CTA loops over tiles and one elected thread streams
-// the next tiles' input boxes [NW rows][C comps][W slots] into a 2-stage
-// shared-memory ring with cp.async.bulk.tensor (TMA, mbarrier completion), so
-// HBM latency overlaps the previous tile's compute.
-// ---------------------------------------------------------------------------
+// TMA tile load (cp.async.bulk.tensor.4d, mbarrier completion) used by the
+// persistent 2-D kernels: box [rows][C comps][32+AL slots] of a SoA buffer.
 __device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map, uint64_t* bar,
                                              int x, int c, int y, int z) {
   asm volatile(
@@ -179,282 +154,6 @@ __device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map, 
       " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(c), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
-}
-
-template <typename T, int V, int NW, int NS = 2>
-struct SmemPT {
-  static constexpr int W = 32 * V, C = 4;
-  // TMA boxes must start 16-byte aligned in x: load AL extra elements from the
-  // aligned-down coordinate and skip `shift` of them when reading
-  static constexpr int AL = 16 / (int)sizeof(T);
-  static constexpr int WB = W + AL;
-  static constexpr int STAGE = NW * C * WB;
-  static constexpr int XY = NW * 2 * C * W;
-  static constexpr int FY = (NW - 1) * C * W;
-  static constexpr size_t bytes() { return (size_t)(NS * STAGE + XY + FY) * sizeof(T) + 64; }
-};
-
-// NS: depth of the TMA ring (tiles in flight ahead of the compute)
-template <typename T, int V, int NW, int MB, int NS = 2>
-__global__ void __launch_bounds__(32 * NW, MB)
-    k_step2d_pt(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
-                int nwin, int ntiles) {
-  constexpr int D = 2, C = 4, W = 32 * V;
-  using SM = SmemPT<T, V, NW, NS>;
-  using VT = typename VecV<T, V>::type;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  T* stage = reinterpret_cast<T*>(smem);
-  T* xy = stage + NS * SM::STAGE;
-  T* fy = xy + SM::XY;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(fy + SM::FY);
-  const Geom& g = a.g;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int SX = (int)g.S[0], SY = (int)g.S[1];
-  const int G = gridDim.x;
-  // programmatic dependent launch: the next step's grid may be scheduled now; it
-  // waits (griddepcontrol.wait below) until this grid has completed and flushed
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NS; ++k) mbar_init(&bar[k], 1);
-    fence_barrier_init();
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-  }
-  // everything above overlaps the previous kernel's tail; nothing it wrote
-  // (state, ghosts, CFL slots) is read before this point
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  Coef<T> kc;
-  if (!step_coef(a, kc)) return;
-  const bool ws = a.cf.dev != nullptr;
-  const T gam = (T)a.cf.gamma;
-  T wmax = T(0);
-  const T gm1 = a.gm1, qx = kc.q[0], nqx = kc.nq2[0], qy = kc.q[1], nqy = kc.nq2[1];
-  __syncthreads();
-  auto issue = [&](int i) {
-    const int tile = blockIdx.x + i * G;
-    if (tile >= ntiles) return;
-    const int s = i % NS;
-    const int w = tile % nwin, yb = tile / nwin;
-    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
-    const int x0 = (int)g.xo + w * (W - 2) - 1;
-    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
-                 (int)g.off[1] + yb * (NW - 2) - 1, 0);
-  };
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NS; ++k) issue(k);
-  }
-  int bad = 0, nan = 0;
-  // loop-invariant addresses (hoisted by hand: the asm barriers/TMA calls in the
-  // loop would otherwise make the compiler recompute them every tile)
-  const unsigned bar_a0 = smem_u32(&bar[0]);
-  const T* const st_lane = stage + warp * C * SM::WB + V * lane;
-  T* const xr_lane = xy + warp * 2 * C * W + V * lane;
-  T* const out_lane = a.out + (int64_t)g.xo + V * lane;
-  // tile t = blockIdx.x + i G  <->  (win, yb) = (t % nwin, t / nwin), advanced
-  // incrementally (no per-tile integer division)
-  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
-  int win = (int)blockIdx.x % nwin, yb = (int)blockIdx.x / nwin;
-  const int nyb = ntiles / nwin;
-  const int64_t cs = g.cstride;
-  for (int i = 0;; ++i) {
-    if (yb >= nyb) break;
-    const int xw = win * (W - 2) - 1;
-    const int yr = yb * (NW - 2) - 1 + warp;
-    const bool row_in = yr <= SY;
-    const bool row_out = (warp >= 1) & (warp <= NW - 2) & (yr < SY);
-    const int s = NS == 2 ? (i & 1) : i % NS;
-    mbar_wait_u32(bar_a0 + 8 * s, (i / NS) & 1);
-    // ---- X
-    T U[V][C], F[V][C], S_[V][C], G_[V][C];
-    {
-      const int sh = ((int)g.xo + xw) % SM::AL;
-      const T* st = st_lane + s * SM::STAGE + sh;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const VT u = *reinterpret_cast<const VT*>(st + c * SM::WB);
-        if constexpr (V == 1) {
-          U[0][c] = u;
-        } else {
-          U[0][c] = u.x;
-          U[1][c] = u.y;
-        }
-      }
-    }
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int xv = xw + V * lane + v;
-      const int b = phys_flux<D, 0>(U[v], F[v], gm1);
-      bad |= ((xv >= -1) & (xv <= SX) & row_in) ? b : 0;
-    }
-    {
-      T Pin[C], Pnx[C], Un[C], Fn[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        Un[c] = __shfl_down_sync(kFull, U[0][c], 1);
-        Fn[c] = __shfl_down_sync(kFull, F[0][c], 1);
-      }
-      force_face<D, 0>(U[V - 1], F[V - 1], Un, Fn, Pnx, qx, nqx, gm1);
-      if constexpr (V == 2) force_face<D, 0>(U[0], F[0], U[1], F[1], Pin, qx, nqx, gm1);
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const T Ppv = __shfl_up_sync(kFull, Pnx[c], 1);
-        if constexpr (V == 2) {
-          S_[0][c] = U[0][c] - (Pin[c] - Ppv);
-          S_[1][c] = U[1][c] - (Pnx[c] - Pin[c]);
-        } else {
-          S_[0][c] = U[0][c] - (Pnx[c] - Ppv);
-        }
-      }
-    }
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int xv = xw + V * lane + v;
-      const int slot = V * lane + v;
-      const int b = phys_flux<D, 1>(S_[v], G_[v], gm1);
-      bad |= ((slot >= 1) & (slot <= W - 2) & (xv < SX) & row_in) ? b : 0;
-    }
-    {
-      T* xr = xr_lane;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        VT sv, gv;
-        if constexpr (V == 1) {
-          sv = S_[0][c];
-          gv = G_[0][c];
-        } else {
-          sv.x = S_[0][c];
-          sv.y = S_[1][c];
-          gv.x = G_[0][c];
-          gv.y = G_[1][c];
-        }
-        *reinterpret_cast<VT*>(xr + c * W) = sv;
-        *reinterpret_cast<VT*>(xr + (C + c) * W) = gv;
-      }
-    }
-    __syncthreads();  // (A) stage s consumed; (U*, F_y) published
-    if (threadIdx.x == 0) {
-      fence_proxy_async();
-      issue(i + NS);
-    }
-    // ---- Y face between rows warp-1 and warp
-    T Py[V][C];
-    if (warp >= 1) {
-      const T* pr = xy + (warp - 1) * 2 * C * W + V * lane;
-      T Sp[V][C], Gp[V][C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const VT sv = *reinterpret_cast<const VT*>(pr + c * W);
-        const VT gv = *reinterpret_cast<const VT*>(pr + (C + c) * W);
-        if constexpr (V == 1) {
-          Sp[0][c] = sv;
-          Gp[0][c] = gv;
-        } else {
-          Sp[0][c] = sv.x;
-          Sp[1][c] = sv.y;
-          Gp[0][c] = gv.x;
-          Gp[1][c] = gv.y;
-        }
-      }
-#pragma unroll
-      for (int v = 0; v < V; ++v) force_face<D, 1>(Sp[v], Gp[v], S_[v], G_[v], Py[v], qy, nqy, gm1);
-      T* fw = fy + (warp - 1) * C * W + V * lane;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        VT pv;
-        if constexpr (V == 1) {
-          pv = Py[0][c];
-        } else {
-          pv.x = Py[0][c];
-          pv.y = Py[1][c];
-        }
-        *reinterpret_cast<VT*>(fw + c * W) = pv;
-      }
-    }
-    __syncthreads();  // (B) y-faces published
-    // ---- update + store
-    if (row_out) {
-      T* dst = out_lane + ((int64_t)((int)g.off[1] + yr) * g.rstride + xw);
-      const T* fu = fy + warp * C * W + V * lane;
-      T o[V][C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const VT pv = *reinterpret_cast<const VT*>(fu + c * W);
-        if constexpr (V == 1) {
-          o[0][c] = S_[0][c] - (pv - Py[0][c]);
-        } else {
-          o[0][c] = S_[0][c] - (pv.x - Py[0][c]);
-          o[1][c] = S_[1][c] - (pv.y - Py[1][c]);
-        }
-      }
-      bool ok[V];
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int slot = V * lane + v;
-        ok[v] = (slot >= 1) & (slot <= W - 2) & (xw + slot < SX);
-      }
-      if constexpr (V == 2) {
-        if (ok[0] & ok[1]) {
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            VT w;
-            w.x = o[0][c];
-            w.y = o[1][c];
-            *reinterpret_cast<VT*>(dst + c * cs) = w;
-          }
-        } else {
-#pragma unroll
-          for (int v = 0; v < V; ++v)
-            if (ok[v])
-#pragma unroll
-              for (int c = 0; c < C; ++c) dst[c * cs + v] = o[v][c];
-        }
-      } else {
-        if (ok[0]) {
-          T* p = dst;
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            *p = o[0][c];
-            p += cs;
-          }
-        }
-      }
-      const bool yface = (yr < g.pad) | (yr >= SY - g.pad);
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        if (ok[v]) {
-          nan = max(nan, max(naninf(o[v][0]), naninf(o[v][C - 1])));
-          if (ws) wmax = fmax(wmax, wavespeed<D>(o[v], gm1, gam));
-          const int xv = xw + V * lane + v;
-          if (yface | (xv < g.pad) | (xv >= SX - g.pad)) images<D, 0>(a, xv, yr, 0, o[v]);
-        }
-      }
-    }
-    win += Gr;
-    yb += Gq;
-    if (win >= nwin) {
-      win -= nwin;
-      ++yb;
-    }
-  }
-  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
-  if (ws) publish_max(a, wmax);
-}
-
-template <typename T, int V, int NW, int MB = (V == 1 ? 2 : 1), int NS = 2>
-static void launch_pt2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
-  constexpr int W = 32 * V;
-  using SM = SmemPT<T, V, NW, NS>;
-  const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
-  const int nyb = (int)((a.g.S[1] + (NW - 2) - 1) / (NW - 2));
-  const int ntiles = nwin * nyb;
-  static int cache[kMaxDevices] = {0};
-  const int per_sm = resident_ctas(k_step2d_pt<T, V, NW, MB, NS>, 32 * NW, SM::bytes(), cache);
-  const int nsm = sm_count();
-  int grid = per_sm * nsm;
-  if (grid > ntiles) grid = ntiles;
-  launch_pdl(k_step2d_pt<T, V, NW, MB, NS>, grid, 32 * NW, SM::bytes(), s, a,
-             *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
 }
 
 // ---------------------------------------------------------------------------
@@ -666,242 +365,20 @@ static void launch_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
 }
 
 
-// Order 2 with adjacent row pairs (P = pd / pk): warp w owns tile rows 2w and
-// 2w+1 of a 2 NW-row tile.  The y-slopes of each row take the partner row from
-// registers (only rows 2w-1 and 2w+2 come from shared memory), the y-face
-// between the two rows is evaluated in registers together with the face below
-// row 2w, and only row 2w+1's evolved upper value and the face below row 2w are
-// handed over.  Same operations per cell and face: bitwise equal to k_step2d_o2.
-template <typename P, int D, int NW, int MB>
-__global__ void __launch_bounds__(32 * NW, MB)
-    k_step2d_o2p(const __grid_constant__ KArgs<typename PairElem<P>::T> a,
-                 const __grid_constant__ CUtensorMap tmap, int nwin, int nyb, int ntiles) {
-  using T = typename PairElem<P>::T;
-  constexpr int C = D + 2, W = 32, R = 2 * NW;
-  using SM = SmemO2<T, R, C>;  // stage geometry of the 2 NW-row box
-  extern __shared__ __align__(1024) unsigned char smem[];
-  T* stage = reinterpret_cast<T*>(smem);
-  T* sx = stage + 2 * SM::STAGE;         // U* of every tile row
-  T* br = sx + R * C * W;                // (Ubar^R_y, F) of row 2w+1, per warp
-  T* fyb = br + NW * 2 * C * W;          // face below row 2w, per warp
-  uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + NW * C * W);
-  const Geom& g = a.g;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j0 = 2 * warp, j1 = j0 + 1;
-  const int wdn = max(warp - 1, 0), wup = min(warp + 1, NW - 1);
-  const int SX = (int)g.S[0], SY = (int)g.S[1];
-  const int G = gridDim.x;
-  Coef<T> kc;
-  if (!step_coef(a, kc)) return;
-  const bool ws = a.cf.dev != nullptr && a.cf.last;
-  const T gam = (T)a.cf.gamma;
-  T wmax = T(0);
-  const P gm1(a.gm1), h2x(kc.h2[0]), h2y(kc.h2[1]), qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]),
-      nqy(kc.nq2[1]);
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  auto issue = [&](int i) {
-    const int tile = blockIdx.x + i * G;
-    if (tile >= ntiles) return;
-    const int s = i & 1;
-    const int w = tile % nwin, r = tile / nwin, yb = r % nyb, zp = r / nyb;
-    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
-    const int x0 = (int)g.xo + w * (W - 4) - 2;
-    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
-                 (int)g.off[1] + yb * (R - 4) - 2, (int)g.off[2] + zp);
-  };
-  if (threadIdx.x == 0) {
-    issue(0);
-    issue(1);
-  }
-  int bad = 0, nan = 0;
-  const bool lane_in = (lane >= 1) & (lane <= 30);
-  const bool lane_out = (lane >= 2) & (lane <= 29);
-  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
-  int win = (int)blockIdx.x % nwin, yq = (int)blockIdx.x / nwin;
-  const int nyz = ntiles / nwin;
-  const int SZ = (int)g.S[2];
-  // rows of a pair that take part in Y1 (1..R-2), Y2 (2..R-2) and the update (2..R-3)
-  const bool y1a = j0 >= 1, y1b = j1 <= R - 2;
-  const bool y2a = j0 >= 2, y2b = j1 >= 2 && j1 <= R - 2;
-  const bool upa = j0 >= 2 && j0 <= R - 3, upb = j1 >= 2 && j1 <= R - 3;
-  for (int i = 0;; ++i) {
-    if (yq >= nyz) break;
-    const int yb = D == 2 ? yq : yq % nyb;
-    const int zp = D == 2 ? 0 : yq / nyb;
-    const int xw = win * (W - 4) - 2;
-    const int yr0 = yb * (R - 4) - 2 + j0, yr1 = yr0 + 1;
-    const int xv = xw + lane;
-    const int s = i & 1;
-    mbar_wait(&bar[s], (i >> 1) & 1);
-    // ---- X (both rows)
-    P S_[C];
-    {
-      P U[C], Um[C], Up[C];
-      const int sh = ((int)g.xo + xw) % SM::AL;
-      const T* r0 = stage + s * SM::STAGE + j0 * C * SM::WB + sh + lane;
-      const T* r1 = r0 + C * SM::WB;
-#pragma unroll
-      for (int c = 0; c < C; ++c) U[c] = P(r0[c * SM::WB], r1[c * SM::WB]);
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        Um[c] = shfl_up1(U[c]);
-        Up[c] = shfl_down1(U[c]);
-      }
-      P bL[C], FbL[C], bR[C], FbR[C];
-      const PkDom b = hancock<D, 0>(Um, U, Up, h2x, gm1, bL, FbL, bR, FbR);
-      const bool xin = lane_in & (xv >= -1) & (xv <= SX);
-      bad |= ((xin & (yr0 <= SY + 1)) ? b.a : 0) | ((xin & (yr1 <= SY + 1)) ? b.b : 0);
-      P Pnx[C];
-      {
-        P bLn[C], FbLn[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          bLn[c] = shfl_down1(bL[c]);
-          FbLn[c] = shfl_down1(FbL[c]);
-        }
-        force_face<D, 0>(bR, FbR, bLn, FbLn, Pnx, qx, nqx, gm1);
-      }
-#pragma unroll
-      for (int c = 0; c < C; ++c) S_[c] = U[c] - (Pnx[c] - shfl_up1(Pnx[c]));
-      T* x0 = sx + j0 * C * W + lane;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        x0[c * W] = S_[c].x;
-        x0[(C + c) * W] = S_[c].y;  // row j1 = j0 + 1 follows row j0 in sx
-      }
-    }
-    __syncthreads();  // (A) stage s consumed; U* published
-    if (threadIdx.x == 0) {
-      fence_proxy_async();
-      issue(i + 2);
-    }
-    // ---- Y1: evolved y boundary values of both rows (partner row from registers)
-    P byL[C], FbyL[C], byR[C], FbyR[C];
-    {
-      const T* rm = sx + max(j0 - 1, 0) * C * W + lane;      // row 2w-1
-      const T* rp = sx + min(j1 + 1, R - 1) * C * W + lane;  // row 2w+2
-      P Sm[C], Sp[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        Sm[c] = P(rm[c * W], S_[c].x);
-        Sp[c] = P(S_[c].y, rp[c * W]);
-      }
-      const PkDom b = hancock<D, 1>(Sm, S_, Sp, h2y, gm1, byL, FbyL, byR, FbyR);
-      const bool xo = lane_out & (xv < SX);
-      bad |= ((xo & y1a & (yr0 >= -1) & (yr0 <= SY)) ? b.a : 0) |
-             ((xo & y1b & (yr1 >= -1) & (yr1 <= SY)) ? b.b : 0);
-      T* w1 = br + warp * 2 * C * W + lane;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        w1[c * W] = byR[c].y;
-        w1[(C + c) * W] = FbyR[c].y;
-      }
-    }
-    __syncthreads();  // (B) Ubar^R_y of rows 2w+1 published
-    // ---- Y2: faces (2w-1 | 2w) and (2w | 2w+1)
-    P Py[C];
-    {
-      const T* r = br + wdn * 2 * C * W + lane;
-      P pR[C], pF[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        pR[c] = P(r[c * W], byR[c].x);
-        pF[c] = P(r[(C + c) * W], FbyR[c].x);
-      }
-      force_face<D, 1>(pR, pF, byL, FbyL, Py, qy, nqy, gm1);
-      T* fw = fyb + warp * C * W + lane;
-#pragma unroll
-      for (int c = 0; c < C; ++c) fw[c * W] = Py[c].x;
-    }
-    (void)y2a;
-    (void)y2b;
-    __syncthreads();  // (C) faces below each pair published
-    // ---- update + store
-    if (lane_out & (xv < SX)) {
-      const T* fu = fyb + wup * C * W + lane;  // face below row 2w+2
-      P o[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) o[c] = S_[c] - (P(Py[c].y, fu[c * W]) - P(Py[c].x, Py[c].y));
-      const int64_t cs = g.cstride;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int yr = h ? yr1 : yr0;
-        if (!(h ? upb : upa) || yr >= SY) continue;
-        T v[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) v[c] = h ? o[c].y : o[c].x;
-        T* dst = a.out + (g.row(yr, zp) * g.rstride + (int)g.xo + xv);
-#pragma unroll
-        for (int c = 0; c < C; ++c) dst[c * cs] = v[c];
-        nan = max(nan, max(naninf(v[0]), naninf(v[C - 1])));
-        if (ws) wmax = fmax(wmax, wavespeed<D>(v, a.gm1, gam));
-        const bool zf = D == 3 && ((zp < g.pad) | (zp >= SZ - g.pad));
-        if ((yr < g.pad) | (yr >= SY - g.pad) | (xv < g.pad) | (xv >= SX - g.pad) | zf)
-          images<D, 0>(a, xv, yr, zp, v);
-      }
-    }
-    win += Gr;
-    yq += Gq;
-    if (win >= nwin) {
-      win -= nwin;
-      ++yq;
-    }
-  }
-  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
-  if (ws) publish_max(a, wmax);
-}
-
-template <typename T, int NW, int MB, int D = 2>
-static void launch_o2p(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
-  using P = typename std::conditional<sizeof(T) == 8, pd, pk>::type;
-  constexpr int W = 32, R = 2 * NW, C = D + 2;
-  using SM = SmemO2<T, R, C>;
-  const size_t bytes = (size_t)(2 * SM::STAGE + R * C * W + NW * 3 * C * W) * sizeof(T) + 64;
-  const int nwin = (int)((a.g.S[0] + (W - 4) - 1) / (W - 4));
-  const int nyb = (int)((a.g.S[1] + (R - 4) - 1) / (R - 4));
-  const int ntiles = nwin * nyb * (D == 3 ? (int)a.g.S[2] : 1);
-  if constexpr (sizeof(T) == 4) pk_set_negzero(s);
-  static int cache[kMaxDevices] = {0};
-  const int per_sm = resident_ctas(k_step2d_o2p<P, D, NW, MB>, 32 * NW, bytes, cache);
-  int grid = per_sm * sm_count();
-  if (grid > ntiles) grid = ntiles;
-  k_step2d_o2p<P, D, NW, MB><<<grid, 32 * NW, bytes, s>>>(
-      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb, ntiles);
-}
-
-// order-2 variants (RPL_VARIANT; box rows = NW)
-static int o2_rows(int variant) {
-  switch (variant) {
-    case 70: return 16;
-    case 71: return 12;
-    case 72: return 12;
-    case 74: return 24;  // row pairs, 12 warps
-    case 75: return 16;  // row pairs, 8 warps x 2 CTAs
-    default: return 24;  // 0 / 73: the default (DESIGN.md tuning log)
-  }
-}
+// Order-2 2-D tile: 24 warps (20 output rows) at one CTA per SM (DESIGN.md tuning log:
+// 16 warps 72.4 us, the row-pair form 68.4 us vs 66.4 us at 1024^2).
+constexpr int kRowsO2 = 24;
 
 int tmap2d_box_o2(const Geom& g, int variant, int* box_w, int* box_rows) {
+  (void)variant;
   *box_w = 32 + 16 / g.elem;
-  *box_rows = o2_rows(variant);
+  *box_rows = kRowsO2;
   return 1;
 }
 
 template <typename T>
 static void launch_step2d_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
-  switch (a.variant) {
-    case 70: return launch_o2<T, 16, 1>(a, tmap, s);
-    case 71: return launch_o2<T, 12, 2>(a, tmap, s);
-    case 72: return launch_o2<T, 12, 1>(a, tmap, s);
-    case 74: return launch_o2p<T, 12, 1>(a, tmap, s);
-    case 75: return launch_o2p<T, 8, 2>(a, tmap, s);
-    default: return launch_o2<T, 24, 1>(a, tmap, s);
-  }
+  launch_o2<T, kRowsO2, 1>(a, tmap, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -1002,25 +479,9 @@ template void launch_xy3d_o2<float>(const KArgs<float>&, const void*, cudaStream
 template void launch_xy3d_o2<double>(const KArgs<double>&, const void*, cudaStream_t);
 
 int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
-  const int al = 16 / g.elem;  // see SmemPT::AL
-  int v = 1, nw = 12;
-  switch (variant) {
-    case 30: nw = 16; break;
-    case 31: v = 2; nw = 8; break;
-    case 32: case 34: case 35: nw = 8; break;
-    case 33: v = 2; nw = 16; break;
-    case 36: v = 2; nw = 8; break;
-    case 38: nw = 10; break;
-    case 44: case 45: case 64: nw = 24; break;
-    case 63: case 65: case 66: nw = 12; break;
-    case 67: nw = 16; break;
-    case 68: nw = 32; break;
-    case 46: nw = 14; break;
-    case 47: nw = 20; break;
-    default: nw = 12; break;  // 0, 37, 39
-  }
-  *box_w = 32 * v + al;
-  *box_rows = nw;
+  (void)variant;
+  *box_w = 32 + 16 / g.elem;  // 16-byte-aligned TMA box start (AL extra elements)
+  *box_rows = kRows2;
   return 1;
 }
 
@@ -1353,44 +814,15 @@ static void launch_ra2d(const KArgs<typename PairElem<P>::T>& a, const void* tma
              *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
 }
 
-// Default 2-D order-1 kernel: adjacent row pairs (k_step2d_ra), 16-row tiles of 8
-// warps, 3 CTAs/SM (variant 67) at every partition size measured: 1024^2 26.9 us
-// (66: 12-row tiles x 4 CTAs 27.2 us; k_step2d_pt 29.1 us); 6400x4000 396 us (64:
-// 24-row tiles x 1 CTA 415 us; 68: 32-row tiles 404 us; k_step2d_pt variant 45 451
-// us) -- profiles/r1/tile_shape_2d.txt, ra2d_variants.txt.
-int auto_variant_2d(const Geom& g) {
-  (void)g;
-  return 67;
-}
-
+// 2-D order-1 kernel: adjacent row pairs (k_step2d_ra), 16-row tiles of 8 warps, 3
+// CTAs/SM at every partition size measured (round 1: 1024^2 26.9 us; 12-row tiles x 4
+// CTAs 27.2 us; the one-row-per-warp form 29.1 us; 6400x4000 396 us vs 24-row tiles x 1
+// CTA 415 us, 32-row 404 us -- profiles/r1/tile_shape_2d.txt, ra2d_variants.txt).
 template <typename T>
 void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   if (a.order == 2) return launch_step2d_o2<T>(a, tmap, s);
-  // k_step2d_pt variants (RPL_VARIANT; DESIGN.md tuning log); box rows = NW
-  switch (a.variant) {
-    case 30: return launch_pt2d<T, 1, 16>(a, tmap, s);
-    case 31: return launch_pt2d<T, 2, 8>(a, tmap, s);
-    case 32: return launch_pt2d<T, 1, 8>(a, tmap, s);
-    case 33: return launch_pt2d<T, 2, 16>(a, tmap, s);
-    case 34: return launch_pt2d<T, 1, 8, 3>(a, tmap, s);
-    case 35: return launch_pt2d<T, 1, 8, 4>(a, tmap, s);
-    case 36: return launch_pt2d<T, 2, 8, 2>(a, tmap, s);
-    case 38: return launch_pt2d<T, 1, 10, 3>(a, tmap, s);
-    case 39: return launch_pt2d<T, 1, 12, 3>(a, tmap, s);
-    case 44: return launch_pt2d<T, 1, 24, 1>(a, tmap, s);
-    case 46: return launch_pt2d<T, 1, 14, 2>(a, tmap, s);
-    case 47: return launch_pt2d<T, 1, 20, 1>(a, tmap, s);
-    case 48: return launch_pt2d<T, 1, 12, 2, 3>(a, tmap, s);  // 3-stage TMA ring
-    case 49: return launch_pt2d<T, 1, 12, 2, 4>(a, tmap, s);  // 4-stage TMA ring
-    case 45: return launch_pt2d<T, 1, 24, 1, 3>(a, tmap, s);
-    case 63: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 6, 2, 2>(a, tmap, s);
-    case 64: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 12, 1, 3>(a, tmap, s);
-    case 65: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 6, 3, 2>(a, tmap, s);
-    case 66: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 6, 4, 2>(a, tmap, s);
-    case 67: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 8, 3, 2>(a, tmap, s);
-    case 68: return launch_ra2d<typename std::conditional<sizeof(T) == 8, pd, pk>::type, 16, 1, 3>(a, tmap, s);
-    default: return launch_pt2d<T, 1, 12, 2>(a, tmap, s);  // 0 / 37: the default
-  }
+  using P = typename std::conditional<sizeof(T) == 8, pd, pk>::type;
+  launch_ra2d<P, kRows2 / 2, 3, 2>(a, tmap, s);
 }
 
 template <typename T>
@@ -1511,302 +943,6 @@ struct SmemFD {
   static constexpr size_t bytes() { return (size_t)(2 * STAGE + UF + FY) * sizeof(T) + 64; }
 };
 
-template <typename T, int NW, int MB>
-__global__ void __launch_bounds__(32 * NW, MB)
-    k_fluxdiff_pt(const __grid_constant__ KArgs<T> a, const __grid_constant__ CUtensorMap tmap,
-                  int nwin, int ntiles) {
-  constexpr int D = 2, C = 4, W = 32;
-  using SM = SmemFD<T, NW>;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  T* stage = reinterpret_cast<T*>(smem);
-  T* uf = stage + 2 * SM::STAGE;
-  T* fyb = uf + SM::UF;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + SM::FY);
-  const Geom& g = a.g;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int SX = (int)g.S[0], SY = (int)g.S[1];
-  const int G = gridDim.x;
-  const T gm1 = a.gm1;
-  const T ilx = T(0.25) / a.q[0], ily = T(0.25) / a.q[1];
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  auto issue = [&](int i) {
-    const int tile = blockIdx.x + i * G;
-    if (tile >= ntiles) return;
-    const int s = i & 1;
-    const int w = tile % nwin, yb = tile / nwin;
-    mbar_arrive_expect_tx(&bar[s], SM::STAGE * (unsigned)sizeof(T));
-    const int x0 = (int)g.xo + w * (W - 2) - 1;
-    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
-                 (int)g.off[1] + yb * (NW - 2) - 1, 0);
-  };
-  if (threadIdx.x == 0) {
-    issue(0);
-    issue(1);
-  }
-  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
-  int win = (int)blockIdx.x % nwin, yb = (int)blockIdx.x / nwin;
-  const int nyb = ntiles / nwin;
-  for (int i = 0;; ++i) {
-    if (yb >= nyb) break;
-    const int xw = win * (W - 2) - 1;
-    const int yr = yb * (NW - 2) - 1 + warp;
-    const int s = i & 1;
-    mbar_wait(&bar[s], (i >> 1) & 1);
-    T U[C], Fx[C], Fy[C], Rx[C];
-    {
-      const int sh = ((int)g.xo + xw) % SM::AL;
-      const T* st = stage + s * SM::STAGE + warp * C * SM::WB + sh + lane;
-#pragma unroll
-      for (int c = 0; c < C; ++c) U[c] = st[c * SM::WB];
-    }
-    phys_flux<D, 0>(U, Fx, gm1);
-    phys_flux<D, 1>(U, Fy, gm1);
-    {
-      T Un[C], Fn[C], Pnx[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        Un[c] = __shfl_down_sync(kFull, U[c], 1);
-        Fn[c] = __shfl_down_sync(kFull, Fx[c], 1);
-      }
-      force_face<D, 0>(U, Fx, Un, Fn, Pnx, a.q[0], a.nq2[0], gm1);
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const T Ppv = __shfl_up_sync(kFull, Pnx[c], 1);
-        Rx[c] = fma(Pnx[c] - Ppv, ilx, T(0));
-      }
-    }
-    {
-      T* w = uf + warp * 2 * C * W + lane;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        w[c * W] = U[c];
-        w[(C + c) * W] = Fy[c];
-      }
-    }
-    __syncthreads();  // (A) stage consumed, (U, F_y) published
-    if (threadIdx.x == 0) {
-      fence_proxy_async();
-      issue(i + 2);
-    }
-    T Py[C];
-    if (warp >= 1) {
-      T Up[C], Fp[C];
-      const T* r = uf + (warp - 1) * 2 * C * W + lane;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        Up[c] = r[c * W];
-        Fp[c] = r[(C + c) * W];
-      }
-      force_face<D, 1>(Up, Fp, U, Fy, Py, a.q[1], a.nq2[1], gm1);
-      T* fw = fyb + warp * C * W + lane;
-#pragma unroll
-      for (int c = 0; c < C; ++c) fw[c * W] = Py[c];
-    }
-    __syncthreads();  // (B) y-faces published
-    if (warp >= 1 && warp <= NW - 2 && yr < SY && lane >= 1 && lane <= 30 && xw + lane < SX) {
-      const T* fu = fyb + (warp + 1) * C * W + lane;
-      T* dst = a.out + ((int64_t)((int)g.off[1] + yr) * g.rstride + (int)g.xo + xw + lane);
-      const int64_t cs = g.cstride;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        *dst = fma(fu[c * W] - Py[c], ily, Rx[c]);
-        dst += cs;
-      }
-    }
-    win += Gr;
-    yb += Gq;
-    if (win >= nwin) {
-      win -= nwin;
-      ++yb;
-    }
-  }
-}
-
-template <typename T, int NW, int MB>
-static void launch_fd_pt(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
-  constexpr int W = 32;
-  using SM = SmemFD<T, NW>;
-  const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
-  const int nyb = (int)((a.g.S[1] + (NW - 2) - 1) / (NW - 2));
-  const int ntiles = nwin * nyb;
-  static int cache[kMaxDevices] = {0};
-  const int per_sm = resident_ctas(k_fluxdiff_pt<T, NW, MB>, 32 * NW, SM::bytes(), cache);
-  const int nsm = sm_count();
-  int grid = per_sm * nsm;
-  if (grid > ntiles) grid = ntiles;
-  k_fluxdiff_pt<T, NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
-      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
-}
-
-
-// fp32: the same tiled flux difference with two tile rows per lane, packed
-// (packed.cuh FFMA2/FADD2).  Warp w owns rows w and w + NW of a 2 NW-row tile
-// (the same TMA box as k_fluxdiff_pt<float, 2 NW>); per lane the operations are
-// k_fluxdiff_pt's, so the result is bitwise that of k_fluxdiff.
-template <int NW, int MB>
-__global__ void __launch_bounds__(32 * NW, MB)
-    k_fluxdiff_rp(const __grid_constant__ KArgs<float> a, const __grid_constant__ CUtensorMap tmap,
-                  int nwin, int ntiles) {
-  constexpr int D = 2, C = 4, W = 32, R = 2 * NW;
-  using SM = SmemFD<float, R>;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  float* stage = reinterpret_cast<float*>(smem);
-  float* uf = stage + 2 * SM::STAGE;
-  float* fyb = uf + SM::UF;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + SM::FY);
-  const Geom& g = a.g;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j0 = warp, j1 = warp + NW;
-  const int SX = (int)g.S[0], SY = (int)g.S[1];
-  const int G = gridDim.x;
-  const pk gm1(a.gm1);
-  const pk ilx(0.25f / a.q[0]), ily(0.25f / a.q[1]);
-  const pk qx(a.q[0]), nqx(a.nq2[0]), qy(a.q[1]), nqy(a.nq2[1]);
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  auto issue = [&](int i) {
-    const int tile = blockIdx.x + i * G;
-    if (tile >= ntiles) return;
-    const int s = i & 1;
-    const int w = tile % nwin, yb = tile / nwin;
-    mbar_arrive_expect_tx(&bar[s], SM::STAGE * 4u);
-    const int x0 = (int)g.xo + w * (W - 2) - 1;
-    tma_load_box(stage + s * SM::STAGE, &tmap, &bar[s], x0 - x0 % SM::AL, 0,
-                 (int)g.off[1] + yb * (R - 2) - 1, 0);
-  };
-  if (threadIdx.x == 0) {
-    issue(0);
-    issue(1);
-  }
-  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
-  int win = (int)blockIdx.x % nwin, yb = (int)blockIdx.x / nwin;
-  const int nyb = ntiles / nwin;
-  const int fb0 = max(j0 - 1, 0);
-  for (int i = 0;; ++i) {
-    if (yb >= nyb) break;
-    const int xw = win * (W - 2) - 1;
-    const int yr0 = yb * (R - 2) - 1 + j0, yr1 = yb * (R - 2) - 1 + j1;
-    const int s = i & 1;
-    mbar_wait(&bar[s], (i >> 1) & 1);
-    pk U[C], Fx[C], Fy[C], Rx[C];
-    {
-      const int sh = ((int)g.xo + xw) % SM::AL;
-      const float* s0 = stage + s * SM::STAGE + j0 * C * SM::WB + sh + lane;
-      const float* s1 = stage + s * SM::STAGE + j1 * C * SM::WB + sh + lane;
-#pragma unroll
-      for (int c = 0; c < C; ++c) U[c] = pk(s0[c * SM::WB], s1[c * SM::WB]);
-    }
-    phys_flux<D, 0>(U, Fx, gm1);
-    phys_flux<D, 1>(U, Fy, gm1);
-    {
-      pk Un[C], Fn[C], Pnx[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        Un[c] = shfl_down1(U[c]);
-        Fn[c] = shfl_down1(Fx[c]);
-      }
-      force_face<D, 0>(U, Fx, Un, Fn, Pnx, qx, nqx, gm1);
-#pragma unroll
-      for (int c = 0; c < C; ++c) Rx[c] = fma(Pnx[c] - shfl_up1(Pnx[c]), ilx, pk(0.0f));
-    }
-    {
-      float* w0 = uf + j0 * 2 * C * W + lane;
-      float* w1 = uf + j1 * 2 * C * W + lane;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        w0[c * W] = U[c].x;
-        w0[(C + c) * W] = Fy[c].x;
-        w1[c * W] = U[c].y;
-        w1[(C + c) * W] = Fy[c].y;
-      }
-    }
-    __syncthreads();  // (A) stage consumed, (U, F_y) published
-    if (threadIdx.x == 0) {
-      fence_proxy_async();
-      issue(i + 2);
-    }
-    pk Py[C];
-    {
-      pk Up[C], Fp[C];
-      const float* r0 = uf + fb0 * 2 * C * W + lane;
-      const float* r1 = uf + (j1 - 1) * 2 * C * W + lane;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        Up[c] = pk(r0[c * W], r1[c * W]);
-        Fp[c] = pk(r0[(C + c) * W], r1[(C + c) * W]);
-      }
-      force_face<D, 1>(Up, Fp, U, Fy, Py, qy, nqy, gm1);
-      float* f0 = fyb + j0 * C * W + lane;
-      float* f1 = fyb + j1 * C * W + lane;
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        if (j0 >= 1) f0[c * W] = Py[c].x;
-        f1[c * W] = Py[c].y;
-      }
-    }
-    __syncthreads();  // (B) y-faces published
-    {
-      const bool xok = lane >= 1 && lane <= 30 && xw + lane < SX;
-      const bool ok0 = xok && j0 >= 1 && yr0 < SY;
-      const bool ok1 = xok && j1 <= R - 2 && yr1 < SY;
-      // face (j | j+1) lives at fyb row j+1 (clamped for the halo row R-1: unused)
-      const float* u0 = fyb + (j0 + 1) * C * W + lane;
-      const float* u1 = fyb + min(j1 + 1, R - 1) * C * W + lane;
-      pk o[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) o[c] = fma(pk(u0[c * W], u1[c * W]) - Py[c], ily, Rx[c]);
-      const int64_t cs = g.cstride;
-      if (ok0) {
-        float* dst = a.out + ((int64_t)((int)g.off[1] + yr0) * g.rstride + (int)g.xo + xw + lane);
-#pragma unroll
-        for (int c = 0; c < C; ++c) dst[c * cs] = o[c].x;
-      }
-      if (ok1) {
-        float* dst = a.out + ((int64_t)((int)g.off[1] + yr1) * g.rstride + (int)g.xo + xw + lane);
-#pragma unroll
-        for (int c = 0; c < C; ++c) dst[c * cs] = o[c].y;
-      }
-    }
-    win += Gr;
-    yb += Gq;
-    if (win >= nwin) {
-      win -= nwin;
-      ++yb;
-    }
-  }
-}
-
-template <int NW, int MB>
-static void launch_fd_rp(const KArgs<float>& a, const void* tmap, cudaStream_t s) {
-  constexpr int W = 32, R = 2 * NW;
-  using SM = SmemFD<float, R>;
-  const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
-  const int nyb = (int)((a.g.S[1] + (R - 2) - 1) / (R - 2));
-  const int ntiles = nwin * nyb;
-  pk_set_negzero(s);
-  static int cache[kMaxDevices] = {0};
-  const int per_sm = resident_ctas(k_fluxdiff_rp<NW, MB>, 32 * NW, SM::bytes(), cache);
-  const int nsm = sm_count();
-  int grid = per_sm * nsm;
-  if (grid > ntiles) grid = ntiles;
-  k_fluxdiff_rp<NW, MB><<<grid, 32 * NW, SM::bytes(), s>>>(
-      a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
-}
-
-
-// fp32 default: adjacent row pairs -- warp w owns rows 2w and 2w+1, the y-face
-// between them is computed in registers together with the face below row 2w
-// (one packed force_face); only row 2w+1's (U, F_y) and that lower face go
-// through shared memory.  Same operations per face and cell: bitwise equal.
 template <int NW, int MB, typename P = pk>
 __global__ void __launch_bounds__(32 * NW, MB)
     k_fluxdiff_ra(const __grid_constant__ KArgs<typename PairElem<P>::T> a,
@@ -1962,19 +1098,11 @@ int fd_tile_rows(int elem) { return 16; }
 
 template <typename T>
 void launch_fluxdiff_tiled(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
-  if constexpr (sizeof(T) == 4) {
-    // packed row pairs (8 warps, the same 16-row box): adjacent rows (default), rows
-    // w, w+8 (78; 73: 3 CTAs/SM); RPL_VARIANT=20: scalar
-    if (a.variant == 20) return launch_fd_pt<T, 16, 2>(a, tmap, s);
-    if (a.variant == 73) return launch_fd_rp<8, 3>(a, tmap, s);
-    if (a.variant == 78) return launch_fd_rp<8, 4>(a, tmap, s);
-    return launch_fd_ra<8, 4>(a, tmap, s);  // adjacent row pairs (default)
-  }
-  if constexpr (sizeof(T) == 8) {
-    if (a.variant == 20) return launch_fd_pt<T, 16, 2>(a, tmap, s);  // fp64 scalar tiles
-    if (a.variant == 79) return launch_fd_ra<8, 3, pd>(a, tmap, s);
-    return launch_fd_ra<8, 2, pd>(a, tmap, s);  // fp64 adjacent row pairs (default)
-  }
+  // adjacent row pairs, 8 warps, 16-row box: fp32 packed (FFMA2) x 4 CTAs/SM, fp64
+  // double pairs x 2 CTAs/SM (round 1: fd8k fp32 561 us, fp64 991 us; the
+  // one-row-per-warp and rows-w,w+8 forms were slower -- profiles/r1/fd_*.txt)
+  if constexpr (sizeof(T) == 4) return launch_fd_ra<8, 4>(a, tmap, s);
+  else return launch_fd_ra<8, 2, pd>(a, tmap, s);
 }
 template void launch_fluxdiff_tiled<float>(const KArgs<float>&, const void*, cudaStream_t);
 template void launch_fluxdiff_tiled<double>(const KArgs<double>&, const void*, cudaStream_t);

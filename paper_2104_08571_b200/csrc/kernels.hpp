@@ -38,6 +38,6 @@ void launch_fluxdiff_tiled(const KArgs<T>& a, const void* tmap, cudaStream_t s);
 int fd_tile_rows(int elem);
 
 int auto_rows_3d(const Geom& g);
-int auto_variant_2d(const Geom& g);  // 2-D order-1 fused tile shape for this partition size
+const char* step3d_kernel_name(int elem, int variant);  // the 3-D step kernel launch_step3d picks
 
 }  // namespace rpl

@@ -242,12 +242,22 @@ struct rpl_domain {
   void* peer_arena[kMaxParts] = {nullptr};  // IPC mappings (to close)
   unsigned long long** d_peer_ctl = nullptr;  // device [nranks]: each rank's control block
   unsigned long long epoch = 0;
+  unsigned nbr_mask = 0;                    // P2P halo neighbours (bit r = rank r)
+  // fault hook (RPL_FAULT_HALO=1, tests only): after every exchange flip the lowest
+  // mantissa bit of rho in one ghost cell per local partition that another partition
+  // sources -- proves the bitwise partition / rank tests can fail
+  int64_t fault_off[kMaxParts];
+  bool fault = false;
   // device-side CFL (rpl_advance_to)
   CflDev* d_cfl = nullptr;
   CflDev* h_cfl = nullptr;  // pinned
   // kernel timing (rpl_profile)
   std::vector<cudaEvent_t> ev;  // pairs
   size_t ev_used = 0;
+  // halo timing (rpl_profile_halo): (interior done = step kernels done, halo ready =
+  // exchange / P2P epoch sync done) pairs, one per exchange, multi-rank only
+  std::vector<cudaEvent_t> evh;
+  size_t evh_used = 0;
 };
 
 static int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
@@ -349,8 +359,11 @@ extern "C" rpl_status rpl_nccl_unique_id(void* out128) {
 
 static void free_events(rpl_domain* d) {
   for (auto e : d->ev) cudaEventDestroy(e);
+  for (auto e : d->evh) cudaEventDestroy(e);
   d->ev.clear();
+  d->evh.clear();
   d->ev_used = 0;
+  d->evh_used = 0;
 }
 
 static void free_domain(rpl_domain* d) {
@@ -418,8 +431,6 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
   CU(cudaMalloc(&d->d_cfl, sizeof(CflDev)));
   CU(cudaMallocHost(&d->h_cfl, sizeof(CflDev)));
   if (const char* v = getenv("RPL_VARIANT")) d->variant = atoi(v);
-  // 2-D order 1: large partitions take the 24-row / 3-stage tile (no wave tail to lose)
-  if (d->variant == 0 && g.D == 2 && g.layout == 0 && c->order == 1) d->variant = auto_variant_2d(g);
   if (g.D == 3) {  // SoA and AoS
     d->tmaps_ok = true;
     for (int p : d->local)
@@ -448,7 +459,35 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
   // 0 = each fused launcher picks its own chunking (2-D); 3-D z-chunk planes:
   if (d->rows <= 0 && g.D == 3) d->rows = auto_rows_3d(g);
   d->p2p = c->nranks > 1 && c->transport == RPL_TRANSPORT_P2P;
-  if (d->p2p) CU(cudaMalloc(&d->d_peer_ctl, sizeof(void*) * kMaxParts));
+  if (d->p2p) {
+    CU(cudaMalloc(&d->d_peer_ctl, sizeof(void*) * kMaxParts));
+    // halo neighbours: ranks whose partitions source a ghost of ours or take one of
+    // ours as a ghost source (one partition per rank; symmetric by construction, the
+    // same global plan on every rank) -- the only ranks a halo epoch waits on
+    std::vector<rpl_halo_edge> plan;
+    build_plan(g, &plan);
+    for (const auto& e : plan) {
+      if (e.src_part == c->rank && e.dst_part != c->rank) d->nbr_mask |= 1u << e.dst_part;
+      if (e.dst_part == c->rank && e.src_part != c->rank) d->nbr_mask |= 1u << e.src_part;
+    }
+  }
+  for (int p = 0; p < kMaxParts; ++p) d->fault_off[p] = -1;
+  if (const char* f = getenv("RPL_FAULT_HALO")) {
+    if (f[0] == '1') {
+      std::vector<rpl_halo_edge> plan;
+      build_plan(g, &plan);
+      for (const auto& e : plan) {
+        const int p = e.dst_part;
+        if (e.src_part == p || d->fault_off[p] >= 0 || !d->buf[0][p]) continue;
+        int pc[3];
+        g.part_coords(p, pc);
+        const int64_t x = e.dst_lo[0] - pc[0] * g.S[0], y = e.dst_lo[1] - pc[1] * g.S[1],
+                      z = e.dst_lo[2] - pc[2] * g.S[2];
+        d->fault_off[p] = g.at(0, x, y, z);  // rho of the first ghost of this edge
+        d->fault = true;
+      }
+    }
+  }
   if (c->nranks > 1 && !d->p2p) {
     if (!g_nccl.load()) return fail(RPL_E_NCCL, "libnccl.so.2 not found (set RPL_NCCL_LIB)");
     ncclUniqueId id;
@@ -686,13 +725,19 @@ static rpl_status exchange_t(rpl_domain* d, int b) {
   return RPL_OK;
 }
 
-// P2P: one warp publishes "rank `me` finished epoch e" into every peer's control
-// block (system-scope release after a system fence, so the step kernel's peer
-// stores are visible first) and waits until every peer published e (acquire).
-// With mode 1 it also publishes the local wavespeed max *smax into slot `me` of
-// the peers' slot set `set` and, after the wait, reduces its own set into *smax
-// (exact: max).  Sets rotate with the step (device CFL): a rank is at most one
-// epoch ahead of any peer, so a set is never rewritten before it was read.
+// P2P: one warp publishes "rank `me` finished epoch e" into the control block of
+// every peer it synchronises with (system-scope release after a system fence, so
+// the step kernel's peer stores are visible first) and waits until each of them
+// published e (acquire).  Mode 0 (halo epoch after a step) involves only the halo
+// neighbours (`peers`, from the halo plan): they are the only ranks whose stores
+// land in our buffers and the only ones whose buffers we store into, so "all
+// neighbours finished step n" is all step n+1 needs -- a rank may run ahead of a
+// non-neighbour by its graph distance, never of a neighbour.  Mode 1 (wavespeed max)
+// involves every rank: it also publishes the local wavespeed max *smax into slot
+// `me` of the peers' slot set `set` and, after the wait, reduces its own set into
+// *smax (exact: max).  Sets rotate with the step (device CFL, one mode-1 sync per
+// step): a rank is at most one epoch ahead of any peer, so a set is never rewritten
+// before it was read.
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -704,11 +749,12 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // the next synchronising call reports it (RPL_E_CUDA).
 __global__ void k_p2p_sync(unsigned long long* const* ctl, int me, int nranks,
                            unsigned long long epoch, unsigned long long* smax, int set, int mode,
-                           unsigned* flag, unsigned long long timeout_ns) {
+                           unsigned* flag, unsigned long long timeout_ns, unsigned peers) {
   const int r = threadIdx.x;
   unsigned long long* mine = ctl[me];
   const int so = kMaxParts * (1 + set);
-  if (r < nranks && r != me) {
+  // mode 0 (halo epoch): the halo neighbours only; mode 1 (wavespeed max): every rank
+  if (r < nranks && r != me && (mode == 1 || ((peers >> r) & 1u))) {
     unsigned long long* peer = ctl[r];
     if (mode == 1) {
       const unsigned long long v = *smax;
@@ -754,7 +800,8 @@ static rpl_status p2p_sync(rpl_domain* d, int mode, unsigned long long* smax = n
     return (unsigned long long)((sec > 0 ? sec : 120.0) * 1e9);
   }();
   k_p2p_sync<<<1, 32, 0, d->stream>>>(d->d_peer_ctl, d->cfg.rank, d->cfg.nranks, d->epoch,
-                                      smax ? smax : d->d_smax, set, mode, d->d_flag, timeout_ns);
+                                      smax ? smax : d->d_smax, set, mode, d->d_flag, timeout_ns,
+                                      d->nbr_mask);
   CU(cudaGetLastError());
   return RPL_OK;
 }
@@ -765,6 +812,15 @@ static rpl_status reduce_max(rpl_domain* d, unsigned long long* slot, int set) {
   if (d->p2p) return p2p_sync(d, 1, slot, set);
   NC(g_nccl.AllReduce(slot, slot, 1, ncclUint64, ncclMax, d->comm, d->stream));
   return RPL_OK;
+}
+
+__global__ void k_fault_flip(unsigned char* p) { p[0] ^= 1u; }
+
+static void inject_fault(rpl_domain* d, int b) {
+  for (int p : d->local)
+    if (d->fault_off[p] >= 0)
+      k_fault_flip<<<1, 1, 0, d->stream>>>((unsigned char*)d->buf[b][p] +
+                                           d->fault_off[p] * d->g.elem);
 }
 
 static rpl_status exchange(rpl_domain* d, int b) {
@@ -880,9 +936,16 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps, const CflArgs*
           if (!st) st = reduce_max(d, &cf->dev->S[sn], 0);
         }
       } else {
+        const bool hprof = d->cfg.nranks > 1 && d->evh_used + 2 <= d->evh.size();
+        if (hprof) cudaEventRecord(d->evh[d->evh_used], d->stream);
         st = exchange(d, nb);
+        if (hprof) {
+          cudaEventRecord(d->evh[d->evh_used + 1], d->stream);
+          d->evh_used += 2;
+        }
       }
       if (st) return st;
+      if (d->fault) inject_fault(d, nb);
       d->cur = nb;  // Listing 8 swap: the current state is the last-written buffer
     }
   }
@@ -1059,7 +1122,27 @@ extern "C" rpl_status rpl_profile(rpl_domain* d, int32_t max_launches) {
     cudaEvent_t e;
     CU(cudaEventCreate(&e));
     d->ev.push_back(e);
+    if (d->cfg.nranks > 1) {
+      CU(cudaEventCreate(&e));
+      d->evh.push_back(e);
+    }
   }
+  return RPL_OK;
+}
+
+extern "C" rpl_status rpl_profile_halo(rpl_domain* d, double* halo_ms, int64_t* exchanges) {
+  if (!d || !halo_ms || !exchanges) return fail(RPL_E_INVALID_ARG, "null argument");
+  CU(cudaSetDevice(d->device));
+  CU(cudaStreamSynchronize(d->stream));
+  double tot = 0.0;
+  for (size_t i = 0; i + 1 < d->evh_used; i += 2) {
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, d->evh[i], d->evh[i + 1]));
+    tot += ms;
+  }
+  *halo_ms = tot;
+  *exchanges = (int64_t)(d->evh_used / 2);
+  d->evh_used = 0;
   return RPL_OK;
 }
 
@@ -1189,6 +1272,21 @@ extern "C" rpl_status rpl_flux_difference(rpl_domain* d, double dt) {
     if (st) return st;
   }
   return d->g.elem == 8 ? fluxdiff_t<double>(d, dt) : fluxdiff_t<float>(d, dt);
+}
+
+extern "C" const char* rpl_kernel_name(const rpl_domain* d, int32_t op) {
+  if (!d) return "";
+  const Geom& g = d->g;
+  if (op == 1) {  // rpl_flux_difference (fluxdiff_t: tiled only for fused 2-D SoA)
+    if (d->cfg.kernel == RPL_KERNEL_FUSED && g.D == 2 && g.layout == 0)
+      return g.elem == 8 ? "k_fluxdiff_ra<pd>" : "k_fluxdiff_ra<pk>";
+    return "k_fluxdiff";
+  }
+  if (op != 0) return "";
+  if (!use_fused(d)) return d->cfg.order == 2 ? "k_sweep2" : "k_sweep";
+  if (d->cfg.order == 2) return g.D == 2 ? "k_step2d_o2" : "k_step2d_o2<3> (x-y) + k_zmarch2 (z)";
+  if (g.D == 2) return g.elem == 8 ? "k_step2d_ra<pd>" : "k_step2d_ra<pk>";
+  return step3d_kernel_name(g.elem, d->variant);
 }
 
 extern "C" rpl_status rpl_get_flux_difference(rpl_domain* d, void* host) {

@@ -232,6 +232,19 @@ class Domain:
         N.check(N.lib().rpl_profile_read(self._h, ctypes.byref(ms), ctypes.byref(n)))
         return ms.value, n.value
 
+    def profile_halo(self):
+        """(summed exposed-halo ms, exchanges) since the last read (multi-rank; the
+        interior-done -> halo-ready event pairs of rpl_profile_halo); synchronises."""
+        ms = ctypes.c_double(0.0)
+        n = ctypes.c_int64(0)
+        N.check(N.lib().rpl_profile_halo(self._h, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
+
+    def kernel_name(self, op: str = "step") -> str:
+        """Name of the kernel rpl_advance ("step") or rpl_flux_difference
+        ("fluxdiff") launches for this configuration."""
+        return N.lib().rpl_kernel_name(self._h, {"step": 0, "fluxdiff": 1}[op]).decode()
+
     @property
     def launches_per_step(self) -> int:
         n = ctypes.c_int32(0)

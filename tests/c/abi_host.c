@@ -21,6 +21,7 @@ int main(void) {
   rpl_config_init(&c);
   CHECK(c.ndim == 1 && c.pad == 2 && c.dtype == RPL_F64 && c.layout == RPL_SOA);
   CHECK(c.gamma == 1.4 && c.nranks == 1 && c.order == 1);
+  CHECK(strcmp(rpl_kernel_name(NULL, 0), "") == 0);
 
   /* BASELINE configs[1]: 2-D 1024^2, pad 2, fp64 */
   c.ndim = 2;

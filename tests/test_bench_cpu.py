@@ -5,6 +5,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -33,3 +35,39 @@ def test_reference_arm_other_ranks_silent():
     env = dict(os.environ, RANK="1", WORLD_SIZE="2")
     out = _run(["--impl", "reference", "--steps", "1", "--warmup", "0"], env=env)
     assert not [l for l in out.strip().splitlines() if l.startswith("{")]
+
+
+def test_gpus_flag_relaunches_under_torchrun():
+    """--gpus 2 without a torchrun environment re-launches bench.py under
+    torch.distributed.run with 2 ranks; rank 0 alone prints one line (reference arm: no
+    GPU needed, so the launch path itself is exercised here)."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = _run(["--impl", "reference", "--workload", "2d1024", "--gpus", "2", "--steps", "1",
+                "--warmup", "0"], env=env)
+    lines = [l for l in out.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+
+
+@pytest.mark.parametrize("wl", ["fd1k", "cfl1024", "o2_1024"])
+def test_reference_arm_runs_the_workload_op(wl):
+    """The reference arm times the same operation as the GPU arm (flux difference, CFL
+    run, order-2 step), not always the order-1 step."""
+    out = _run(["--impl", "reference", "--workload", wl, "--steps", "1", "--warmup", "0"])
+    d = json.loads([l for l in out.strip().splitlines() if l.startswith("{")][0])
+    op = {"fd1k": "fluxdiff", "cfl1024": "cfl", "o2_1024": "step"}[wl]
+    assert f"op={op}" in d["config"]["sample"] and d["value"] > 0
+    if wl == "fd1k":
+        assert d["unit"] == "Gcell/s"
+
+
+def test_weak_2d_decomposition_grows_x_and_y():
+    """2-D weak scaling as the paper runs it: per-GPU size fixed, the
+    domain grows in x and y, split along y."""
+    import bench
+    for n in (1, 2, 4, 8):
+        gn, parts = bench.decomposition(bench.WORKLOADS["2d1024"], n)
+        assert parts == [1, n] and gn[0] * gn[1] == n * 1024 * 1024 and gn[1] % n == 0
+    assert bench.decomposition(bench.WORKLOADS["2d1024"], 4)[0] == [2048, 2048]

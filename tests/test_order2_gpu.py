@@ -129,12 +129,10 @@ def test_order2_is_more_accurate_on_smooth_data():
     assert errs[1] < 0.2 * errs[0], errs
 
 
-@pytest.mark.parametrize("variant", ["0", "70", "71", "74", "75"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_order2_2d_variants_bitwise(variant, dtype, monkeypatch):
-    """2-D order-2 fused kernels (RPL_VARIANT: 0 = default; 70/71 = other tile
-    shapes; 74/75 = adjacent row pairs, 12 warps / 8 warps x 2 CTAs) give the split
-    kernel's bit pattern (ragged windows and tiles, mixed boundaries)."""
+def test_order2_2d_fused_bitwise(dtype):
+    """The 2-D order-2 fused kernel gives the split kernel's bit pattern (ragged
+    windows and tiles, mixed boundaries)."""
     from test_parity_gpu import bits_equal
     n = (130, 61)
     dx = [1.0 / 130] * 2
@@ -144,5 +142,4 @@ def test_order2_2d_variants_bitwise(variant, dtype, monkeypatch):
     dt = 0.4 * dx[0] / 5.8
     kw = dict(dx=dx, bc_lo=["reflective", "periodic"], bc_hi=["clamp", "periodic"])
     ref = gpu(U0, dt, 6, dtype=dtype, kernel="split", **kw)
-    monkeypatch.setenv("RPL_VARIANT", variant)
     assert bits_equal(gpu(U0, dt, 6, dtype=dtype, **kw), ref)

@@ -21,9 +21,10 @@ def _port():
     return p
 
 
-def _rank(rank, world, port, n, parts, kw, steps, q, t_end=None):
+def _rank(rank, world, port, n, parts, kw, steps, q, t_end=None, env=None):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(env or {})
     import torch
     import torch.distributed as dist
 
@@ -169,22 +170,40 @@ def test_p2p_stalled_peer_times_out():
     assert dt < 60
 
 
-def _check(n, parts, kw, t_end):
+def _run_ranks(n, parts, kw, t_end, steps=6, env=None):
     world = int(np.prod(parts))
-    steps = 6
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank, args=(r, world, port, n, parts, kw, steps, q, t_end))
+    procs = [ctx.Process(target=_rank, args=(r, world, port, n, parts, kw, steps, q, t_end, env))
              for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
     for p in procs:
         p.join(timeout=120)
+    return res
+
+
+def _check(n, parts, kw, t_end):
+    steps = 6
+    res = _run_ranks(n, parts, kw, t_end, steps)
     ref, s_ref = _single(n, kw, steps, t_end)
     D = len(n)
     for rank, lo, hi, out, s in res:
         assert s == s_ref
         sl = tuple(slice(lo[d], hi[d]) for d in reversed(range(D)))
         assert np.array_equal(out, ref[sl]), rank
+
+
+@pytest.mark.parametrize("n,parts,kw", [((130, 64), (1, 2), {}), ((40, 32, 24), (2, 2, 1), {})])
+def test_p2p_fault_hook_turns_bitwise_test_red(n, parts, kw):
+    """RPL_FAULT_HALO=1 flips one mantissa bit of one halo ghost per rank after every
+    exchange: the rank-vs-single bit-identity check must then fail (it is not blind)."""
+    steps = 6
+    res = _run_ranks(n, parts, kw, None, steps, env={"RPL_FAULT_HALO": "1"})
+    ref, _ = _single(n, kw, steps)
+    D = len(n)
+    same = [np.array_equal(out, ref[tuple(slice(lo[d], hi[d]) for d in reversed(range(D)))])
+            for _, lo, hi, out, _ in res]
+    assert not all(same)

@@ -2,8 +2,9 @@
 """Summarise ncu reports (--page raw) into a short text table + traffic JSON.
 
 usage: python tools/ncu_summary.py OUT_DIR key=report.ncu-rep [key=report.ncu-rep ...]
-Writes OUT_DIR/ncu_<key>.txt and merges {key: dram bytes per launch} into
-profiles/ncu_traffic.json (read by bench.py for roofline.traffic).
+Writes OUT_DIR/ncu_<key>.txt and merges {key: {bytes: dram bytes per launch, kernel,
+capture: that summary file, date: capture date}} into profiles/ncu_traffic.json
+(read by bench.py for roofline.traffic and roofline.traffic_source).
 """
 import csv
 import io
@@ -11,6 +12,7 @@ import json
 import os
 import subprocess
 import sys
+import time
 
 METRICS = [
     ("gpu__time_duration.sum", "duration"),
@@ -64,7 +66,9 @@ def main():
                      ", ".join(f"{n}={int(c)}" for c, n in stalls))
         if "dram__bytes_read.sum" in got:
             b = to_bytes(*got["dram__bytes_read.sum"]) + to_bytes(*got["dram__bytes_write.sum"])
-            traffic[key] = b
+            when = time.strftime("%Y-%m-%d", time.gmtime(os.path.getmtime(rep)))
+            traffic[key] = {"bytes": b, "kernel": kname.split("(")[0],
+                            "capture": os.path.join(out_dir, f"ncu_{key}.txt"), "date": when}
             lines.append(f"  dram bytes read+write per launch: {b:.4e}")
         open(os.path.join(out_dir, f"ncu_{key}.txt"), "w").write("\n".join(lines) + "\n")
         print("\n".join(lines))
