@@ -82,7 +82,22 @@ typedef enum { RPL_KERNEL_FUSED = 0, RPL_KERNEL_SPLIT = 1 } rpl_kernel;
  *        wait is bounded: a peer that does not arrive within RPL_P2P_TIMEOUT_S
  *        seconds (environment, default 120) makes the next synchronising call
  *        return RPL_E_CUDA instead of hanging. */
-typedef enum { RPL_TRANSPORT_NCCL = 0, RPL_TRANSPORT_P2P = 1 } rpl_transport;
+/* Halo transport.  NCCL (nranks > 1): the step kernel runs on the partition's shell
+ * tiles (halo sources) first; a side stream packs the halo slabs (one kernel),
+ * exchanges them with grouped ncclSend/ncclRecv and unpacks them while the interior
+ * tiles run; the next step waits only for that (sec. 5.4.1).
+ * P2P (nranks > 1): the step kernel stores halo cells straight into the neighbours'
+ * buffers over NVLink (CUDA IPC, rpl_p2p_export/attach) and a one-warp kernel syncs
+ * with the halo neighbours.  LOOPBACK (nranks == 1, prod(parts) > 1): the local
+ * partitions exchange halos through the NCCL path's pack -> transfer -> unpack
+ * kernels and side stream, with a device copy instead of send/recv (the single-GPU
+ * test of that choreography); otherwise partitions of one rank write each other's
+ * ghosts directly. */
+typedef enum {
+  RPL_TRANSPORT_NCCL = 0,
+  RPL_TRANSPORT_P2P = 1,
+  RPL_TRANSPORT_LOOPBACK = 2
+} rpl_transport;
 
 typedef struct {
   int32_t ndim;            /* 1, 2 or 3 */
@@ -106,7 +121,8 @@ typedef struct {
   void* arena;             /* optional caller-owned device memory of rpl_arena_bytes() bytes */
   int32_t rows_per_chunk;  /* fused kernels: rows (2-D) / planes (3-D) marched per warp task;
                               0 -> automatic */
-  rpl_transport transport; /* nranks > 1: NCCL (default) or P2P */
+  rpl_transport transport; /* nranks > 1: NCCL (default) or P2P; nranks == 1: LOOPBACK
+                              (optional, multi-partition) */
   int32_t order;           /* reconstruction order (the paper's Listing 8 is
                               order 1, reading S7): 1 = piecewise constant (default);
                               2 = MUSCL-Hancock with minmod slopes + FORCE (Toro's SLIC,

@@ -18,7 +18,7 @@ STATUS = {0: "RPL_OK", -1: "RPL_E_INVALID_ARG", -2: "RPL_E_NOT_DIVISIBLE",
 F32, F64 = 0, 1
 SOA, AOS = 0, 1
 FUSED, SPLIT = 0, 1
-TRANSPORT_NCCL, TRANSPORT_P2P = 0, 1
+TRANSPORT_NCCL, TRANSPORT_P2P, TRANSPORT_LOOPBACK = 0, 1, 2
 BC_TRANSMISSIVE, BC_PERIODIC, BC_REFLECTIVE = 0, 1, 2
 MAP_TRANSLATE, MAP_REFLECT, MAP_BROADCAST = 0, 1, 2
 
@@ -101,7 +101,7 @@ def lib():
     L.rpl_last_error.argtypes = []
     L.rpl_last_error.restype = ctypes.c_char_p
     for name in EXPORTS:
-        if name not in ("rpl_config_init", "rpl_destroy", "rpl_last_error"):
+        if name not in ("rpl_config_init", "rpl_destroy", "rpl_last_error", "rpl_kernel_name"):
             getattr(L, name).restype = st
     _lib = L
     return L

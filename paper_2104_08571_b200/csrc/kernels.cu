@@ -672,9 +672,11 @@ __global__ void __launch_bounds__(32 * NW, MB)
   T wmax = T(0);
   const P gm1(a.gm1), qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]), nqy(kc.nq2[1]);
   __syncthreads();
+  const int* tl = a.tiles;  // tile list (shell-first halo overlap) or nullptr: every tile
   auto issue = [&](int i) {
-    const int tile = blockIdx.x + i * G;
-    if (tile >= ntiles) return;
+    const int idx = blockIdx.x + i * G;
+    if (idx >= ntiles) return;
+    const int tile = tl ? tl[idx] : idx;
     const int s = i % NS;
     const int w = tile % nwin, yb = tile / nwin;
     mbar_arrive_expect_tx(&bar[s], STAGE * (unsigned)sizeof(T));
@@ -689,11 +691,18 @@ __global__ void __launch_bounds__(32 * NW, MB)
   int bad = 0, nan = 0;
   const unsigned bar_a0 = smem_u32(&bar[0]);
   const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
-  int win = (int)blockIdx.x % nwin, yb = (int)blockIdx.x / nwin;
   const int nyb = ntiles / nwin;
+  int idx = (int)blockIdx.x, win = 0, yb = 0;
+  bool live;
+  if (tl) {
+    live = idx < ntiles;
+    if (live) win = tl[idx] % nwin, yb = tl[idx] / nwin;
+  } else {
+    win = idx % nwin, yb = idx / nwin;
+    live = yb < nyb;
+  }
   const int64_t cs = g.cstride;
-  for (int i = 0;; ++i) {
-    if (yb >= nyb) break;
+  for (int i = 0; live; ++i) {
     const int xw = win * (W - 2) - 1;
     const int yr0 = yb * (R - 2) - 1 + j0, yr1 = yr0 + 1;
     const int xv = xw + lane;
@@ -785,11 +794,18 @@ __global__ void __launch_bounds__(32 * NW, MB)
         if (xface | (yr < g.pad) | (yr >= SY - g.pad)) images<D, 0>(a, xv, yr, 0, v);
       }
     }
-    win += Gr;
-    yb += Gq;
-    if (win >= nwin) {
-      win -= nwin;
-      ++yb;
+    if (tl) {
+      idx += G;
+      live = idx < ntiles;
+      if (live) win = tl[idx] % nwin, yb = tl[idx] / nwin;
+    } else {
+      win += Gr;
+      yb += Gq;
+      if (win >= nwin) {
+        win -= nwin;
+        ++yb;
+      }
+      live = yb < nyb;
     }
   }
   if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
@@ -804,7 +820,8 @@ static void launch_ra2d(const KArgs<typename PairElem<P>::T>& a, const void* tma
   const size_t bytes = (size_t)(NS * R * C * (W + AL) + NW * 3 * C * W) * sizeof(T) + 64;
   const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((a.g.S[1] + (R - 2) - 1) / (R - 2));
-  const int ntiles = nwin * nyb;
+  const int ntiles = a.tiles ? a.ntiles : nwin * nyb;
+  if (ntiles <= 0) return;
   if constexpr (sizeof(T) == 4) pk_set_negzero(s);
   static int cache[kMaxDevices] = {0};
   const int per_sm = resident_ctas(k_step2d_ra<P, NW, MB, NS>, 32 * NW, bytes, cache);

@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
   uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + SM::FY);
   const Geom& g = a.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int t = blockIdx.x;
+  int t = a.tiles ? a.tiles[blockIdx.x] : (int)blockIdx.x;
   const int win = t % nwin;
   t /= nwin;
   const int yb = t % nyb;
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
   uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + SM::FY);
   const Geom& g = a.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int t = blockIdx.x;
+  int t = a.tiles ? a.tiles[blockIdx.x] : (int)blockIdx.x;
   const int win = t % nwin;
   t /= nwin;
   const int yb = t % nyb;
@@ -588,11 +588,13 @@ static int launch3_rb(const KArgs<typename PairElem<P>::T>& a, const void* tmap,
   const int nwin = (int)((g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((g.S[1] + TY - 1) / TY);
   const int nzc = (int)((g.S[2] + a.rows - 1) / a.rows);
+  const int grid = a.tiles ? a.ntiles : nwin * nyb * nzc;
+  if (grid <= 0) return 0;
   const size_t sm = SmemRB<NW, T, NS>::bytes();
   if constexpr (sizeof(T) == 4) pk_set_negzero(s);
   static int cache[kMaxDevices] = {0};
   resident_ctas(k_step3d_rb<NW, MB, L, P, NS>, 32 * NW, sm, cache);
-  k_step3d_rb<NW, MB, L, P, NS><<<nwin * nyb * nzc, 32 * NW, sm, s>>>(
+  k_step3d_rb<NW, MB, L, P, NS><<<grid, 32 * NW, sm, s>>>(
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb);
   return 0;
 }
@@ -606,11 +608,13 @@ static int launch3_sp(const KArgs<typename PairElem<P>::T>& a, const void* tmap,
   const int nwin = (int)((g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((g.S[1] + TY - 1) / TY);
   const int nzc = (int)((g.S[2] + a.rows - 1) / a.rows);
+  const int grid = a.tiles ? a.ntiles : nwin * nyb * nzc;
+  if (grid <= 0) return 0;
   const size_t sm = SmemRB<NW, T, NS>::bytes();
   if constexpr (sizeof(T) == 4) pk_set_negzero(s);
   static int cache[kMaxDevices] = {0};
   resident_ctas(k_step3d_sp<NW, MB, L, P, NS>, 32 * NW, sm, cache);
-  k_step3d_sp<NW, MB, L, P, NS><<<nwin * nyb * nzc, 32 * NW, sm, s>>>(
+  k_step3d_sp<NW, MB, L, P, NS><<<grid, 32 * NW, sm, s>>>(
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, nyb);
   return 0;
 }

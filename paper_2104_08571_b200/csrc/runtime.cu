@@ -62,6 +62,7 @@ struct Nccl {
   decltype(&ncclGroupEnd) GroupEnd = nullptr;
   decltype(&ncclAllReduce) AllReduce = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  decltype(&ncclCommInitRankConfig) CommInitRankConfig = nullptr;  // optional (maxCTAs)
   bool load() {
     if (tried) return ok;
     tried = true;
@@ -81,6 +82,7 @@ struct Nccl {
     RPL_SYM(GroupEnd);
     RPL_SYM(AllReduce);
     RPL_SYM(GetErrorString);
+    RPL_SYM(CommInitRankConfig);
 #undef RPL_SYM
     ok = GetUniqueId && CommInitRank && CommDestroy && Send && Recv && GroupStart && GroupEnd &&
          AllReduce && GetErrorString;
@@ -150,6 +152,71 @@ __global__ void k_edge(const Geom g, const DevEdge e, T* buf, T* msg, int dir) {
       store_cell<D, L>(g, buf, l[0], l[1], l[2], v);
     }
   }
+}
+
+// All edges of one exchange direction in one launch (blockIdx.y = edge): pack (dir
+// 0) reads the source partition's buffer tab[e.src_part], unpack (dir 1) writes
+// tab[e.dst_part]; e.offset is the edge's element offset in msg.  Same cell map,
+// flips and message layout as k_edge.
+template <typename T, int D, int L>
+__global__ void k_edges(const Geom g, const DevEdge* __restrict__ edges, T* const* tab, T* msg,
+                        int dir) {
+  const DevEdge& e = edges[blockIdx.y];
+  T* buf = tab[dir == 0 ? e.src_part : e.dst_part];
+  T* m = msg + e.offset;
+  const int64_t ex = e.dst_hi[0] - e.dst_lo[0], ey = e.dst_hi[1] - e.dst_lo[1];
+  int pcs[3], pcd[3];
+  g.part_coords(e.src_part, pcs);
+  g.part_coords(e.dst_part, pcd);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e.count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t[3] = {e.dst_lo[0] + i % ex, e.dst_lo[1] + (i / ex) % ey,
+                          e.dst_lo[2] + i / (ex * ey)};
+    T v[D + 2];
+    if (dir == 0) {
+      int64_t sc[3];
+      bool flip[3] = {false, false, false};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int64_t k = t[d] - e.dst_lo[d];
+        sc[d] = e.mode[d] == RPL_MAP_TRANSLATE ? e.src_lo[d] + k
+                : e.mode[d] == RPL_MAP_REFLECT ? e.src_hi[d] - 1 - k
+                                               : e.src_lo[d];
+        flip[d] = e.mode[d] == RPL_MAP_REFLECT;
+        sc[d] -= (d < D) ? (int64_t)pcs[d] * g.S[d] : 0;
+      }
+#pragma unroll
+      for (int c = 0; c < D + 2; ++c) v[c] = buf[g.at(c, sc[0], sc[1], sc[2])];
+#pragma unroll
+      for (int d = 0; d < D; ++d)
+        if (flip[d]) v[1 + d] = -v[1 + d];
+#pragma unroll
+      for (int c = 0; c < D + 2; ++c) m[c * e.count + i] = v[c];
+    } else {
+      int64_t l[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) l[d] = t[d] - ((d < D) ? (int64_t)pcd[d] * g.S[d] : 0);
+#pragma unroll
+      for (int c = 0; c < D + 2; ++c) v[c] = m[c * e.count + i];
+      store_cell<D, L>(g, buf, l[0], l[1], l[2], v);
+    }
+  }
+}
+
+template <typename T>
+void launch_edges(const Geom& g, const DevEdge* edges, int nedges, int64_t max_count,
+                  T* const* tab, T* msg, int dir, cudaStream_t s) {
+  if (nedges <= 0) return;
+  int gx = (int)((max_count + 255) / 256);
+  const int cap = (148 * 8 + nedges - 1) / nedges;
+  if (gx > cap) gx = cap;
+  if (gx < 1) gx = 1;
+  const dim3 grid(gx, nedges);
+#define RPL_E(DD, LL) k_edges<T, DD, LL><<<grid, 256, 0, s>>>(g, edges, tab, msg, dir)
+  if (g.D == 1) { if (g.layout == 0) RPL_E(1, 0); else RPL_E(1, 1); }
+  if (g.D == 2) { if (g.layout == 0) RPL_E(2, 0); else RPL_E(2, 1); }
+  if (g.D == 3) { if (g.layout == 0) RPL_E(3, 0); else RPL_E(3, 1); }
+#undef RPL_E
 }
 
 // interior <-> dense SoA staging [C][S2][S1][S0] (AoS layout transfers)
@@ -223,6 +290,21 @@ struct rpl_domain {
   std::vector<Peer> send_peers, recv_peers;
   void* d_send = nullptr;
   void* d_recv = nullptr;
+  // message exchange (xmode 1: NCCL between ranks; 2: loopback between the local
+  // partitions of one rank through the same pack -> transfer -> unpack path, device
+  // copies instead of send/recv): flat edge lists with absolute message offsets
+  int xmode = 0;
+  DevEdge* d_sedges = nullptr;
+  DevEdge* d_redges = nullptr;
+  int n_sedges = 0, n_redges = 0;
+  int64_t max_scount = 0, max_rcount = 0, n_selems = 0, n_relems = 0;
+  void** d_tab_self = nullptr;  // loopback: [2][kMaxParts] tables holding one partition each
+  // shell-first overlap (fused order-1 kernels): per local partition the tiles whose
+  // cells are halo sources (shell) then the rest (interior), in d_tiles
+  int* d_tiles = nullptr;
+  int tile_off[kMaxParts] = {0}, n_shell[kMaxParts] = {0}, n_inter[kMaxParts] = {0};
+  cudaStream_t xstream = nullptr;  // side stream of the exchange (high priority)
+  cudaEvent_t ev_shell = nullptr, ev_halo = nullptr;
   int rows = 0;
   int variant = 0;
   // 3-D fused kernel: one TMA descriptor per (buffer, local partition)
@@ -243,9 +325,10 @@ struct rpl_domain {
   unsigned long long** d_peer_ctl = nullptr;  // device [nranks]: each rank's control block
   unsigned long long epoch = 0;
   unsigned nbr_mask = 0;                    // P2P halo neighbours (bit r = rank r)
-  // fault hook (RPL_FAULT_HALO=1, tests only): after every exchange flip the lowest
-  // mantissa bit of rho in one ghost cell per local partition that another partition
-  // sources -- proves the bitwise partition / rank tests can fail
+  // fault hook (RPL_FAULT_HALO=1, tests only): after every exchange flip one mantissa
+  // bit (relative 2^-20) of rho in one ghost cell next to the interior, per local
+  // partition that another partition sources -- proves the bitwise partition / rank
+  // tests can fail
   int64_t fault_off[kMaxParts];
   bool fault = false;
   // device-side CFL (rpl_advance_to)
@@ -299,8 +382,11 @@ static rpl_status geom_of(const rpl_config* c, Geom* g) {
   if (c->nranks > 1 && c->nranks != g->nparts)
     return fail(RPL_E_INVALID_ARG, "nranks must be 1 or prod(parts) (one partition per rank)");
   if (c->rank < 0 || c->rank >= c->nranks) return fail(RPL_E_INVALID_ARG, "rank out of range");
-  if (c->transport != RPL_TRANSPORT_NCCL && c->transport != RPL_TRANSPORT_P2P)
+  if (c->transport != RPL_TRANSPORT_NCCL && c->transport != RPL_TRANSPORT_P2P &&
+      c->transport != RPL_TRANSPORT_LOOPBACK)
     return fail(RPL_E_INVALID_ARG, "transport");
+  if (c->transport == RPL_TRANSPORT_LOOPBACK && c->nranks != 1)
+    return fail(RPL_E_INVALID_ARG, "LOOPBACK transport is for one rank (local partitions)");
   if (c->nranks > 1 && c->transport == RPL_TRANSPORT_NCCL && !c->nccl_id)
     return fail(RPL_E_INVALID_ARG, "nccl_id required");
   if (c->nranks > 32 && c->transport == RPL_TRANSPORT_P2P)
@@ -384,8 +470,159 @@ static void free_domain(rpl_domain* d) {
   if (d->stage) cudaFree(d->stage);
   if (d->d_send) cudaFree(d->d_send);
   if (d->d_recv) cudaFree(d->d_recv);
+  if (d->d_sedges) cudaFree(d->d_sedges);
+  if (d->d_redges && d->d_redges != d->d_sedges) cudaFree(d->d_redges);
+  if (d->d_tab_self) cudaFree(d->d_tab_self);
+  if (d->d_tiles) cudaFree(d->d_tiles);
+  if (d->ev_shell) cudaEventDestroy(d->ev_shell);
+  if (d->ev_halo) cudaEventDestroy(d->ev_halo);
+  if (d->xstream) cudaStreamDestroy(d->xstream);
   if (d->own_stream && d->stream) cudaStreamDestroy(d->stream);
   delete d;
+}
+
+
+// Message exchange plan (xmode 1: NCCL, 2: loopback): one flat edge list per
+// direction, edges grouped per peer (NCCL) in plan order, absolute element offsets
+// into the send / recv arenas; and, for the fused order-1 kernels, each local
+// partition's tiles split into shell (some cell is a halo source) and interior.
+static rpl_status setup_exchange(rpl_domain* d) {
+  const Geom& g = d->g;
+  const rpl_config* c = &d->cfg;
+  std::vector<rpl_halo_edge> plan;
+  build_plan(g, &plan);
+  auto dev_edge = [&](const rpl_halo_edge& e) {
+    DevEdge de;
+    memset(&de, 0, sizeof(de));
+    for (int k = 0; k < 3; ++k) {
+      de.src_lo[k] = e.src_lo[k];
+      de.src_hi[k] = e.src_hi[k];
+      de.dst_lo[k] = e.dst_lo[k];
+      de.dst_hi[k] = e.dst_hi[k];
+      de.mode[k] = e.mode[k];
+    }
+    de.src_part = e.src_part;
+    de.dst_part = e.dst_part;
+    de.count = (e.dst_hi[0] - e.dst_lo[0]) * (e.dst_hi[1] - e.dst_lo[1]) *
+               (e.dst_hi[2] - e.dst_lo[2]);
+    return de;
+  };
+  std::vector<DevEdge> se, re;
+  if (d->xmode == 1) {
+    const int me = c->rank;
+    auto add = [&](std::vector<Peer>& peers, int peer, const rpl_halo_edge& e) {
+      Peer* P = nullptr;
+      for (auto& q : peers)
+        if (q.rank == peer) P = &q;
+      if (!P) {
+        peers.push_back(Peer());
+        P = &peers.back();
+        P->rank = peer;
+      }
+      DevEdge de = dev_edge(e);
+      de.offset = P->elems;
+      P->elems += de.count * g.C;
+      P->edges.push_back(de);
+    };
+    for (const auto& e : plan) {
+      if (e.src_part == me && e.dst_part != me) add(d->send_peers, e.dst_part, e);
+      if (e.dst_part == me && e.src_part != me) add(d->recv_peers, e.src_part, e);
+    }
+    int64_t ns = 0, nr = 0;
+    for (auto& P : d->send_peers) {
+      P.offset = ns;
+      ns += P.elems;
+      for (auto e : P.edges) { e.offset += P.offset; se.push_back(e); }
+    }
+    for (auto& P : d->recv_peers) {
+      P.offset = nr;
+      nr += P.elems;
+      for (auto e : P.edges) { e.offset += P.offset; re.push_back(e); }
+    }
+    d->n_selems = ns;
+    d->n_relems = nr;
+  } else {
+    int64_t off = 0;  // loopback: one message list, packed and unpacked in place order
+    for (const auto& e : plan)
+      if (e.src_part != e.dst_part) {
+        DevEdge de = dev_edge(e);
+        de.offset = off;
+        off += de.count * g.C;
+        se.push_back(de);
+      }
+    re = se;
+    d->n_selems = d->n_relems = off;
+    // step kernels write ghost images into their own partition only: the other
+    // partitions' halos travel through the messages
+    std::vector<void*> tabs(2 * (size_t)kMaxParts * kMaxParts, nullptr);
+    for (int b = 0; b < 2; ++b)
+      for (int p : d->local) tabs[((size_t)b * kMaxParts + p) * kMaxParts + p] = d->buf[b][p];
+    CU(cudaMalloc(&d->d_tab_self, sizeof(void*) * tabs.size()));
+    CU(cudaMemcpy(d->d_tab_self, tabs.data(), sizeof(void*) * tabs.size(),
+                  cudaMemcpyHostToDevice));
+  }
+  for (const auto& e : se) d->max_scount = std::max(d->max_scount, e.count);
+  for (const auto& e : re) d->max_rcount = std::max(d->max_rcount, e.count);
+  d->n_sedges = (int)se.size();
+  d->n_redges = (int)re.size();
+  if (d->n_selems) CU(cudaMalloc(&d->d_send, d->n_selems * g.elem));
+  if (d->n_relems) CU(cudaMalloc(&d->d_recv, d->n_relems * g.elem));
+  if (!se.empty()) {
+    CU(cudaMalloc(&d->d_sedges, sizeof(DevEdge) * se.size()));
+    CU(cudaMemcpy(d->d_sedges, se.data(), sizeof(DevEdge) * se.size(), cudaMemcpyHostToDevice));
+  }
+  if (d->xmode == 2) {
+    d->d_redges = d->d_sedges;
+  } else if (!re.empty()) {
+    CU(cudaMalloc(&d->d_redges, sizeof(DevEdge) * re.size()));
+    CU(cudaMemcpy(d->d_redges, re.data(), sizeof(DevEdge) * re.size(), cudaMemcpyHostToDevice));
+  }
+  int lo_prio = 0, hi_prio = 0;
+  CU(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  CU(cudaStreamCreateWithPriority(&d->xstream, cudaStreamNonBlocking, hi_prio));
+  CU(cudaEventCreateWithFlags(&d->ev_shell, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&d->ev_halo, cudaEventDisableTiming));
+  // shell / interior tiles of the fused order-1 kernels (2-D SoA, 3-D)
+  if (g.D >= 2 && c->order == 1 && (g.D == 3 || g.layout == 0)) {
+    const int64_t wx = kTileX, wy = kTileY, wz = g.D == 3 ? d->rows : 1;
+    const int64_t nx = (g.S[0] + wx - 1) / wx, ny = (g.S[1] + wy - 1) / wy,
+                  nz = g.D == 3 ? (g.S[2] + wz - 1) / wz : 1;
+    std::vector<int> all;
+    for (int p : d->local) {
+      int pc[3];
+      g.part_coords(p, pc);
+      std::vector<char> shell((size_t)(nx * ny * nz), 0);
+      for (const auto& e : se) {
+        if (e.src_part != p) continue;
+        int64_t lo[3], hi[3];  // local source box (all pad layers the plan sends)
+        for (int k = 0; k < 3; ++k) {
+          const int64_t o = k < g.D ? (int64_t)pc[k] * g.S[k] : 0;
+          lo[k] = e.src_lo[k] - o;
+          hi[k] = e.src_hi[k] - o;
+        }
+        for (int64_t tz = 0; tz < nz; ++tz)
+          for (int64_t ty = 0; ty < ny; ++ty)
+            for (int64_t tx = 0; tx < nx; ++tx) {
+              const int64_t a0[3] = {tx * wx, ty * wy, tz * wz};
+              const int64_t a1[3] = {a0[0] + wx, a0[1] + wy, g.D == 3 ? a0[2] + wz : 1};
+              bool hit = true;
+              for (int k = 0; k < 3; ++k) hit &= a0[k] < hi[k] && lo[k] < a1[k];
+              if (hit) shell[(size_t)((tz * ny + ty) * nx + tx)] = 1;
+            }
+      }
+      d->tile_off[p] = (int)all.size();
+      for (int64_t t = 0; t < nx * ny * nz; ++t)
+        if (shell[(size_t)t]) all.push_back((int)t);
+      d->n_shell[p] = (int)all.size() - d->tile_off[p];
+      for (int64_t t = 0; t < nx * ny * nz; ++t)
+        if (!shell[(size_t)t]) all.push_back((int)t);
+      d->n_inter[p] = (int)all.size() - d->tile_off[p] - d->n_shell[p];
+    }
+    CU(cudaMalloc(&d->d_tiles, sizeof(int) * std::max<size_t>(all.size(), 1)));
+    if (!all.empty())
+      CU(cudaMemcpy(d->d_tiles, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice));
+  }
+  return RPL_OK;
 }
 
 static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
@@ -481,56 +718,49 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
         if (e.src_part == p || d->fault_off[p] >= 0 || !d->buf[0][p]) continue;
         int pc[3];
         g.part_coords(p, pc);
-        const int64_t x = e.dst_lo[0] - pc[0] * g.S[0], y = e.dst_lo[1] - pc[1] * g.S[1],
-                      z = e.dst_lo[2] - pc[2] * g.S[2];
-        d->fault_off[p] = g.at(0, x, y, z);  // rho of the first ghost of this edge
+        // a face edge (one dim outside the partition): its ghost layer next to the
+        // interior, mid-face in the other dims -- a cell the next step reads
+        int64_t q[3];
+        int outside = 0;
+        for (int k = 0; k < 3; ++k) {
+          const int64_t o = k < g.D ? (int64_t)pc[k] * g.S[k] : 0;
+          const int64_t lo = e.dst_lo[k] - o, hi = e.dst_hi[k] - o;
+          if (k < g.D && hi <= 0) {
+            q[k] = -1;
+            ++outside;
+          } else if (k < g.D && lo >= g.S[k]) {
+            q[k] = g.S[k];
+            ++outside;
+          } else {
+            q[k] = (lo + hi - 1) / 2;
+          }
+        }
+        if (outside != 1) continue;
+        d->fault_off[p] = g.at(0, q[0], q[1], q[2]);  // rho of that ghost
         d->fault = true;
       }
     }
   }
-  if (c->nranks > 1 && !d->p2p) {
+  d->xmode = (c->nranks > 1 && !d->p2p) ? 1
+             : (c->nranks == 1 && c->transport == RPL_TRANSPORT_LOOPBACK && g.nparts > 1) ? 2
+                                                                                         : 0;
+  if (d->xmode == 1) {
     if (!g_nccl.load()) return fail(RPL_E_NCCL, "libnccl.so.2 not found (set RPL_NCCL_LIB)");
     ncclUniqueId id;
     memcpy(&id, c->nccl_id, sizeof(id));
-    NC(g_nccl.CommInitRank(&d->comm, c->nranks, id, c->rank));
-    std::vector<rpl_halo_edge> plan;
-    build_plan(g, &plan);
-    const int me = c->rank;
-    auto add = [&](std::vector<Peer>& peers, int peer, const rpl_halo_edge& e) {
-      Peer* P = nullptr;
-      for (auto& q : peers)
-        if (q.rank == peer) P = &q;
-      if (!P) {
-        peers.push_back(Peer());
-        P = &peers.back();
-        P->rank = peer;
-      }
-      DevEdge de;
-      memset(&de, 0, sizeof(de));
-      for (int k = 0; k < 3; ++k) {
-        de.src_lo[k] = e.src_lo[k];
-        de.src_hi[k] = e.src_hi[k];
-        de.dst_lo[k] = e.dst_lo[k];
-        de.dst_hi[k] = e.dst_hi[k];
-        de.mode[k] = e.mode[k];
-      }
-      de.src_part = e.src_part;
-      de.dst_part = e.dst_part;
-      de.count = (e.dst_hi[0] - e.dst_lo[0]) * (e.dst_hi[1] - e.dst_lo[1]) *
-                 (e.dst_hi[2] - e.dst_lo[2]);
-      de.offset = P->elems;
-      P->elems += de.count * g.C;
-      P->edges.push_back(de);
-    };
-    for (const auto& e : plan) {
-      if (e.src_part == me && e.dst_part != me) add(d->send_peers, e.dst_part, e);
-      if (e.dst_part == me && e.src_part != me) add(d->recv_peers, e.src_part, e);
+    if (g_nccl.CommInitRankConfig) {
+      // cap NCCL's CTAs: the interior step kernel keeps the SMs while halos move
+      ncclConfig_t cc = NCCL_CONFIG_INITIALIZER;
+      const char* m = getenv("RPL_NCCL_MAX_CTAS");
+      cc.maxCTAs = m ? atoi(m) : 8;
+      NC(g_nccl.CommInitRankConfig(&d->comm, c->nranks, id, c->rank, &cc));
+    } else {
+      NC(g_nccl.CommInitRank(&d->comm, c->nranks, id, c->rank));
     }
-    int64_t ns = 0, nr = 0;
-    for (auto& P : d->send_peers) { P.offset = ns; ns += P.elems; }
-    for (auto& P : d->recv_peers) { P.offset = nr; nr += P.elems; }
-    if (ns) CU(cudaMalloc(&d->d_send, ns * g.elem));
-    if (nr) CU(cudaMalloc(&d->d_recv, nr * g.elem));
+  }
+  if (d->xmode) {
+    rpl_status st = setup_exchange(d);
+    if (st) return st;
   }
   CU(cudaStreamSynchronize(d->stream));
   return RPL_OK;
@@ -705,22 +935,27 @@ extern "C" rpl_status rpl_get_padded(rpl_domain* d, int32_t part, void* host) {
   return RPL_OK;
 }
 
+// Halo messages of buffer b on stream st: pack every send edge (one kernel) ->
+// grouped ncclSend/ncclRecv (xmode 1) or one device copy (loopback) -> unpack every
+// receive edge (one kernel).
 template <typename T>
-static rpl_status exchange_t(rpl_domain* d, int b) {
+static rpl_status exchange_t(rpl_domain* d, int b, cudaStream_t st) {
   const Geom& g = d->g;
-  T* mine = (T*)d->buf[b][d->cfg.rank];
-  for (auto& P : d->send_peers)
-    for (auto& e : P.edges) launch_edge<T>(g, e, mine, (T*)d->d_send + P.offset + e.offset, 0, d->stream);
+  T* const* tab = (T* const*)(d->d_tab + b * kMaxParts);
+  launch_edges<T>(g, d->d_sedges, d->n_sedges, d->max_scount, tab, (T*)d->d_send, 0, st);
   CU(cudaGetLastError());
-  const ncclDataType_t ty = g.elem == 8 ? ncclFloat64 : ncclFloat32;
-  NC(g_nccl.GroupStart());
-  for (auto& P : d->send_peers)
-    NC(g_nccl.Send((T*)d->d_send + P.offset, P.elems, ty, P.rank, d->comm, d->stream));
-  for (auto& P : d->recv_peers)
-    NC(g_nccl.Recv((T*)d->d_recv + P.offset, P.elems, ty, P.rank, d->comm, d->stream));
-  NC(g_nccl.GroupEnd());
-  for (auto& P : d->recv_peers)
-    for (auto& e : P.edges) launch_edge<T>(g, e, mine, (T*)d->d_recv + P.offset + e.offset, 1, d->stream);
+  if (d->xmode == 1) {
+    const ncclDataType_t ty = g.elem == 8 ? ncclFloat64 : ncclFloat32;
+    NC(g_nccl.GroupStart());
+    for (auto& P : d->send_peers)
+      NC(g_nccl.Send((T*)d->d_send + P.offset, P.elems, ty, P.rank, d->comm, st));
+    for (auto& P : d->recv_peers)
+      NC(g_nccl.Recv((T*)d->d_recv + P.offset, P.elems, ty, P.rank, d->comm, st));
+    NC(g_nccl.GroupEnd());
+  } else if (d->n_selems) {
+    CU(cudaMemcpyAsync(d->d_recv, d->d_send, d->n_selems * g.elem, cudaMemcpyDeviceToDevice, st));
+  }
+  launch_edges<T>(g, d->d_redges, d->n_redges, d->max_rcount, tab, (T*)d->d_recv, 1, st);
   CU(cudaGetLastError());
   return RPL_OK;
 }
@@ -814,19 +1049,24 @@ static rpl_status reduce_max(rpl_domain* d, unsigned long long* slot, int set) {
   return RPL_OK;
 }
 
-__global__ void k_fault_flip(unsigned char* p) { p[0] ^= 1u; }
+// flip mantissa bit 20 from the top (relative change 2^-20 -- a 1-ulp flip can be
+// absorbed by rounding where the flux does not depend on rho, e.g. at rest)
+__global__ void k_fault_flip(unsigned char* p, int elem) {
+  if (elem == 8) p[4] ^= 1u;   // bit 32 of the double
+  else p[0] ^= 8u;             // bit 3 of the float
+}
 
 static void inject_fault(rpl_domain* d, int b) {
   for (int p : d->local)
     if (d->fault_off[p] >= 0)
       k_fault_flip<<<1, 1, 0, d->stream>>>((unsigned char*)d->buf[b][p] +
-                                           d->fault_off[p] * d->g.elem);
+                                           d->fault_off[p] * d->g.elem, d->g.elem);
 }
 
 static rpl_status exchange(rpl_domain* d, int b) {
-  if (d->cfg.nranks <= 1) return RPL_OK;
   if (d->p2p) return p2p_sync(d, 0);  // halos were stored by the step kernel itself
-  return d->g.elem == 8 ? exchange_t<double>(d, b) : exchange_t<float>(d, b);
+  if (!d->xmode) return RPL_OK;       // one partition, or partitions writing each other's ghosts
+  return d->g.elem == 8 ? exchange_t<double>(d, b, d->stream) : exchange_t<float>(d, b, d->stream);
 }
 
 template <typename T>
@@ -838,7 +1078,8 @@ static rpl_status fill_t(rpl_domain* d) {
   T* const* tab = (T* const*)(d->d_tab + d->cur * kMaxParts);
   for (int p : d->local) launch_fill<T>(d->g, p, tab, d->stream);
   CU(cudaGetLastError());
-  if (d->p2p) return RPL_OK;  // k_fill read the peers' interiors directly
+  // P2P / one rank (loopback included): k_fill read the sources' interiors directly
+  if (d->p2p || d->cfg.nranks == 1) return RPL_OK;
   return exchange(d, d->cur);
 }
 
@@ -859,6 +1100,13 @@ static bool use_fused(const rpl_domain* d) {
          ((d->g.D == 2 && d->g.layout == 0) || (d->g.D == 3 && d->tmaps_ok));
 }
 
+// shell-first overlap of the message exchange (NCCL / loopback) with the interior
+// tiles: fused order-1 kernels with tile lists, fixed dt (the device-CFL step
+// combines the wavespeed after the whole step)
+static bool overlapped(const rpl_domain* d) {
+  return d->xmode && d->d_tiles && use_fused(d) && d->cfg.order == 1;
+}
+
 // kernel passes per step: fused = 1 (3-D order 2: x-y pass + z pass), split = D
 static int passes(const rpl_domain* d) {
   if (!use_fused(d)) return d->g.D;
@@ -868,10 +1116,11 @@ static int passes(const rpl_domain* d) {
 extern "C" rpl_status rpl_launches_per_step(const rpl_domain* d, int32_t* out) {
   if (!d || !out) return fail(RPL_E_INVALID_ARG, "null argument");
   int n = (int)d->local.size() * passes(d);
-  int ne = 0;
-  for (auto& P : d->send_peers) ne += (int)P.edges.size();
-  for (auto& P : d->recv_peers) ne += (int)P.edges.size();
-  n += ne * passes(d);
+  if (d->xmode) {
+    n += ((d->n_sedges > 0) + (d->n_redges > 0)) * passes(d);  // pack + unpack kernels
+    if (overlapped(d))  // shell and interior launches of the step kernel
+      for (int p : d->local) n += (d->n_shell[p] > 0 && d->n_inter[p] > 0) ? 1 : 0;
+  }
   if (d->p2p) n += passes(d);  // one flag kernel per exchange
   *out = n;
   return RPL_OK;
@@ -900,48 +1149,79 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps, const CflArgs*
   if (cf) a.cf = *cf;
   const bool fused = use_fused(d);
   const bool xyz = fused && g.D == 3 && d->cfg.order == 2;  // x-y pass, then z pass
+  const bool ov = overlapped(d) && !cf;  // shell tiles -> side-stream exchange || interior
+  const bool hx = d->cfg.nranks > 1 || d->xmode;  // this domain exchanges halos
+  // one step-kernel launch for partition p (sweep sw; tiles: optional tile list)
+  auto launch = [&](int p, int sw, int nb, const int* tiles, int ntiles) {
+    a.part = p;
+    g.part_coords(p, a.pc);
+    for (int k = 0; k < 3; ++k) a.lo[k] = a.pc[k] * g.S[k];
+    a.in = (const T*)d->buf[d->cur][p];
+    a.out = (T*)d->buf[nb][p];
+    a.outs = d->xmode == 2 ? (T* const*)(d->d_tab_self + ((size_t)nb * kMaxParts + p) * kMaxParts)
+                           : (T* const*)(d->d_tab + nb * kMaxParts);
+    a.tiles = tiles;
+    a.ntiles = ntiles;
+    const bool prof = d->ev_used + 2 <= d->ev.size();
+    if (prof) cudaEventRecord(d->ev[d->ev_used], d->stream);
+    if (xyz && sw == 0) launch_xy3d_o2<T>(a, d->tmap[d->cur][p].b, d->stream);
+    else if (xyz) launch_zmarch2<T>(a, d->stream);
+    else if (fused && g.D == 2) launch_step2d<T>(a, d->tmap[d->cur][p].b, d->stream);
+    else if (fused) launch_step3d<T>(a, d->tmap[d->cur][p].b, d->stream);
+    else launch_sweep<T>(a, sw, d->stream);
+    if (prof) {
+      cudaEventRecord(d->ev[d->ev_used + 1], d->stream);
+      d->ev_used += 2;
+    }
+  };
   for (int s = 0; s < nsteps; ++s) {
     const int nsweep = passes(d);
     if (cf) a.cf.step = cf->step + s;
     for (int sw = 0; sw < nsweep; ++sw) {
       const int nb = d->cur ^ 1;
       a.cf.last = sw == nsweep - 1;
-      a.outs = (T* const*)(d->d_tab + nb * kMaxParts);
-      for (int p : d->local) {
-        a.part = p;
-        g.part_coords(p, a.pc);
-        for (int k = 0; k < 3; ++k) a.lo[k] = a.pc[k] * g.S[k];
-        a.in = (const T*)d->buf[d->cur][p];
-        a.out = (T*)d->buf[nb][p];
-        const bool prof = d->ev_used + 2 <= d->ev.size();
-        if (prof) cudaEventRecord(d->ev[d->ev_used], d->stream);
-        if (xyz && sw == 0) launch_xy3d_o2<T>(a, d->tmap[d->cur][p].b, d->stream);
-        else if (xyz) launch_zmarch2<T>(a, d->stream);
-        else if (fused && g.D == 2) launch_step2d<T>(a, d->tmap[d->cur][p].b, d->stream);
-        else if (fused) launch_step3d<T>(a, d->tmap[d->cur][p].b, d->stream);
-        else launch_sweep<T>(a, sw, d->stream);
-        if (prof) {
-          cudaEventRecord(d->ev[d->ev_used + 1], d->stream);
-          d->ev_used += 2;
-        }
-      }
-      CU(cudaGetLastError());
-      rpl_status st;
-      if (cf && a.cf.last && d->cfg.nranks > 1) {
-        const int sn = (a.cf.step + 1) % 3;
-        if (d->p2p) {
-          st = p2p_sync(d, 1, &cf->dev->S[sn], 1 + sn);  // halo epoch + wavespeed in one sync
-        } else {
-          st = exchange(d, nb);
-          if (!st) st = reduce_max(d, &cf->dev->S[sn], 0);
-        }
-      } else {
-        const bool hprof = d->cfg.nranks > 1 && d->evh_used + 2 <= d->evh.size();
-        if (hprof) cudaEventRecord(d->evh[d->evh_used], d->stream);
-        st = exchange(d, nb);
+      rpl_status st = RPL_OK;
+      const bool hprof = hx && d->evh_used + 2 <= d->evh.size();
+      if (ov) {
+        // shell tiles first; the side stream packs, exchanges and unpacks their halo
+        // cells while the interior tiles run; the next step waits for the halos only
+        for (int p : d->local)
+          if (d->n_shell[p]) launch(p, sw, nb, d->d_tiles + d->tile_off[p], d->n_shell[p]);
+        CU(cudaGetLastError());
+        CU(cudaEventRecord(d->ev_shell, d->stream));
+        CU(cudaStreamWaitEvent(d->xstream, d->ev_shell, 0));
+        st = d->g.elem == 8 ? exchange_t<double>(d, nb, d->xstream)
+                            : exchange_t<float>(d, nb, d->xstream);
+        if (st) return st;
+        if (hprof) cudaEventRecord(d->evh[d->evh_used + 1], d->xstream);  // halo ready
+        CU(cudaEventRecord(d->ev_halo, d->xstream));
+        for (int p : d->local)
+          if (d->n_inter[p])
+            launch(p, sw, nb, d->d_tiles + d->tile_off[p] + d->n_shell[p], d->n_inter[p]);
+        CU(cudaGetLastError());
         if (hprof) {
-          cudaEventRecord(d->evh[d->evh_used + 1], d->stream);
+          cudaEventRecord(d->evh[d->evh_used], d->stream);  // interior done
           d->evh_used += 2;
+        }
+        CU(cudaStreamWaitEvent(d->stream, d->ev_halo, 0));
+      } else {
+        for (int p : d->local) launch(p, sw, nb, nullptr, 0);
+        CU(cudaGetLastError());
+        if (cf && a.cf.last && d->cfg.nranks > 1) {
+          const int sn = (a.cf.step + 1) % 3;
+          if (d->p2p) {
+            st = p2p_sync(d, 1, &cf->dev->S[sn], 1 + sn);  // halo epoch + wavespeed in one sync
+          } else {
+            st = exchange(d, nb);
+            if (!st) st = reduce_max(d, &cf->dev->S[sn], 0);
+          }
+        } else {
+          if (hprof) cudaEventRecord(d->evh[d->evh_used], d->stream);
+          st = exchange(d, nb);
+          if (hprof) {
+            cudaEventRecord(d->evh[d->evh_used + 1], d->stream);
+            d->evh_used += 2;
+          }
         }
       }
       if (st) return st;
@@ -1122,7 +1402,7 @@ extern "C" rpl_status rpl_profile(rpl_domain* d, int32_t max_launches) {
     cudaEvent_t e;
     CU(cudaEventCreate(&e));
     d->ev.push_back(e);
-    if (d->cfg.nranks > 1) {
+    if (d->cfg.nranks > 1 || d->xmode) {
       CU(cudaEventCreate(&e));
       d->evh.push_back(e);
     }
@@ -1138,7 +1418,7 @@ extern "C" rpl_status rpl_profile_halo(rpl_domain* d, double* halo_ms, int64_t* 
   for (size_t i = 0; i + 1 < d->evh_used; i += 2) {
     float ms = 0.f;
     CU(cudaEventElapsedTime(&ms, d->evh[i], d->evh[i + 1]));
-    tot += ms;
+    tot += ms > 0.f ? ms : 0.f;  // overlapped: the halos may be ready before the interior
   }
   *halo_ms = tot;
   *exchanges = (int64_t)(d->evh_used / 2);

@@ -57,7 +57,8 @@ def make_config(size, pad=2, parts=None, dtype="f64", layout="soa", kernel="fuse
     cfg.stream = int(stream) if stream else None
     cfg.arena = int(arena) if arena else None
     cfg.rows_per_chunk = int(rows_per_chunk)
-    cfg.transport = {"nccl": N.TRANSPORT_NCCL, "p2p": N.TRANSPORT_P2P}[transport]
+    cfg.transport = {"nccl": N.TRANSPORT_NCCL, "p2p": N.TRANSPORT_P2P,
+                     "loopback": N.TRANSPORT_LOOPBACK}[transport]
     cfg.order = int(order)
     return cfg
 

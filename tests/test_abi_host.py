@@ -40,6 +40,8 @@ def test_library_exports_every_header_symbol():
     (dict(size=(10, 8), gamma=1.0), -1),
     (dict(size=(10, 8), nranks=3), -1),
     (dict(size=(16, 16), parts=(2, 2), nranks=4, rank=1), -1),  # missing nccl id
+    (dict(size=(16, 16), parts=(2, 2), nranks=4, rank=1, nccl_id=b"x" * 128,
+          transport="loopback"), -1),                           # loopback is one rank
 ])
 def test_config_errors(kw, status):
     with pytest.raises(N.RplError) as ei:
@@ -49,6 +51,7 @@ def test_config_errors(kw, status):
 
 def test_config_ok_and_arena():
     R.config_check(size=(1024, 1024), pad=2)
+    R.config_check(size=(64, 64), parts=(2, 2), transport="loopback")
     n = R.arena_bytes(size=(1024, 1024), pad=2, dtype="f64")
     # two padded buffers, C=4 comps, pitch >= 1024 + ghosts, rows 1028
     assert 2 * 4 * 1028 * 1030 * 8 <= n <= 2 * 4 * 1028 * 1152 * 8 + 4096
@@ -159,3 +162,10 @@ def test_plain_c_consumer(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=60)
     assert out.returncode == 0, out.stderr
     assert out.stdout.strip() == "ok"
+
+
+def test_kernel_name_binding_returns_string():
+    """rpl_kernel_name returns a C string (bytes through ctypes), "" for a null domain."""
+    from paper_2104_08571_b200 import _native as N
+    assert N.lib().rpl_kernel_name(None, 0) == b""
+    assert N.lib().rpl_kernel_name(None, 1) == b""

@@ -506,9 +506,9 @@ def test_zero_steps_and_repeated_calls_compose():
     assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("n,parts", [((190, 126), (2, 3)), ((40, 33, 24), (1, 2, 2))])
+@pytest.mark.parametrize("n,parts", [((190, 126), (2, 3)), ((40, 34, 24), (1, 2, 2))])
 def test_fault_hook_turns_partition_bitwise_red(n, parts, monkeypatch):
-    """RPL_FAULT_HALO=1 (tests only) flips the lowest mantissa bit of rho in one halo
+    """RPL_FAULT_HALO=1 (tests only) flips one mantissa bit (2^-20 relative) of rho in one halo
     ghost of every partition after each step: the multi-partition vs one-partition bit
     identity must break (the bitwise tests can fail), while a one-partition run (no halo
     exchange) is untouched."""
