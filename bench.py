@@ -281,7 +281,7 @@ def _oracle_rate(wl, g, U, dt, threads, budget_s, cells):
         t0 = time.perf_counter()
         _oracle_run(wl, g, U, dt, 1)
         one = time.perf_counter() - t0
-        k = max(1, min(60, int(budget_s / max(one, 1e-6))))
+        k = max(1, min(1000, int(budget_s / max(one, 1e-6))))
         t0 = time.perf_counter()
         _oracle_run(wl, g, U, dt, k)
         el = time.perf_counter() - t0

@@ -321,6 +321,7 @@ struct rpl_domain {
                                             // sets 1-3: device CFL, rotated by step)
   int64_t base_off = 0;                     // arena -> 256-aligned buffer base
   bool p2p = false, p2p_attached = false;
+  bool p2p_broken = false;                  // a peer missed an epoch (sticky, see check_flag)
   void* peer_arena[kMaxParts] = {nullptr};  // IPC mappings (to close)
   unsigned long long** d_peer_ctl = nullptr;  // device [nranks]: each rank's control block
   unsigned long long epoch = 0;
@@ -886,7 +887,8 @@ static rpl_status xfer(rpl_domain* d, void* host, bool to_dev, int which = -1) {
 static rpl_status check_flag(rpl_domain* d) {
   CU(cudaMemcpyAsync(d->h_flag, d->d_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, d->stream));
   CU(cudaStreamSynchronize(d->stream));
-  if (*d->h_flag & 2u)
+  if (*d->h_flag & 2u) d->p2p_broken = true;  // the epoch protocol cannot recover
+  if (d->p2p_broken)
     return fail(RPL_E_CUDA, "P2P transport: a peer rank did not reach the step epoch within "
                             "RPL_P2P_TIMEOUT_S (default 120 s)");
   if (*d->h_flag)
@@ -899,9 +901,16 @@ extern "C" rpl_status rpl_set_state(rpl_domain* d, const void* host) {
   CU(cudaSetDevice(d->device));
   rpl_status st = xfer(d, (void*)host, true);
   if (st) return st;
+  // a new state clears the domain-error bit (bit 0); a P2P timeout (bit 1) is sticky
+  // for the domain's lifetime (p2p_broken), so it is read before the flag is reset
+  CU(cudaMemcpyAsync(d->h_flag, d->d_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, d->stream));
+  CU(cudaStreamSynchronize(d->stream));
+  if (*d->h_flag & 2u) d->p2p_broken = true;
   CU(cudaMemsetAsync(d->d_flag, 0, sizeof(unsigned), d->stream));
   CU(cudaStreamSynchronize(d->stream));
   d->ghosts_stale = true;
+  if (d->p2p_broken)
+    return fail(RPL_E_CUDA, "P2P transport: an earlier step epoch timed out (RPL_P2P_TIMEOUT_S)");
   return RPL_OK;
 }
 
@@ -1028,6 +1037,8 @@ __global__ void k_p2p_sync(unsigned long long* const* ctl, int me, int nranks,
 static rpl_status p2p_sync(rpl_domain* d, int mode, unsigned long long* smax = nullptr,
                            int set = 0) {
   if (!d->p2p_attached) return fail(RPL_E_INVALID_ARG, "P2P transport: call rpl_p2p_attach first");
+  if (d->p2p_broken)
+    return fail(RPL_E_CUDA, "P2P transport: an earlier step epoch timed out (RPL_P2P_TIMEOUT_S)");
   ++d->epoch;
   static const unsigned long long timeout_ns = [] {
     const char* e = getenv("RPL_P2P_TIMEOUT_S");

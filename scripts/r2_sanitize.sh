@@ -12,8 +12,8 @@ for tool in memcheck racecheck synccheck; do
   done
 done
 # P2P transport: two ranks (processes) on one GPU, flag kernel + peer stores
-timeout 900 $CS --tool memcheck --target-processes all --error-exitcode 9 python -m pytest tests/test_p2p_gpu.py -q -x -k "bitwise_equal_single_rank and 130" > $OUT/memcheck_p2p.log 2>&1
+timeout 900 $CS --tool memcheck --target-processes all --error-exitcode 9 python -m pytest tests/test_p2p_gpu.py -q -x -k "test_p2p_ranks_bitwise_equal_single_rank and n0" > $OUT/memcheck_p2p.log 2>&1
 echo "memcheck p2p rc=$?" >> $OUT/summary.txt
-timeout 900 $CS --tool synccheck --target-processes all --error-exitcode 9 python -m pytest tests/test_p2p_gpu.py -q -x -k "bitwise_equal_single_rank and 130" > $OUT/synccheck_p2p.log 2>&1
+timeout 900 $CS --tool synccheck --target-processes all --error-exitcode 9 python -m pytest tests/test_p2p_gpu.py -q -x -k "test_p2p_ranks_bitwise_equal_single_rank and n0" > $OUT/synccheck_p2p.log 2>&1
 echo "synccheck p2p rc=$?" >> $OUT/summary.txt
 cat $OUT/summary.txt

@@ -344,9 +344,10 @@ def test_flux_difference_tiled_equals_plain_bitwise(dtype, n, pad, parts):
     assert bits_equal(out[0], out[1])
 
 
+@pytest.mark.parametrize("variant", ["0"])
 @pytest.mark.parametrize("parts", [(1, 1), (2, 3)])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_2d_fused_bitwise(parts, dtype):
+def test_2d_fused_bitwise(parts, dtype, variant, monkeypatch):
     """The 2-D fused kernel gives bitwise the split kernel's result (ragged windows and
     tiles, partitions)."""
     n = (190, 126)
@@ -356,6 +357,7 @@ def test_2d_fused_bitwise(parts, dtype):
         U0 = U0.astype(np.float32)
     dt = 0.4 * dx[0] / 5.8
     ref = run_gpu(U0, dt, 7, dtype=dtype, kernel="split", dx=dx, parts=parts)
+    monkeypatch.setenv("RPL_VARIANT", variant)
     assert bits_equal(run_gpu(U0, dt, 7, dtype=dtype, dx=dx, parts=parts), ref)
 
 
