@@ -44,11 +44,22 @@ WORKLOADS = {
                  label="3-D Euler FORCE 256^3 (BASELINE configs[4])"),
     # the paper's own 2-D scaling problems
     "p6400": dict(ndim=2, n=(6400, 4000), dtype="f64", scaling="strong",
-                  label="2-D Euler FORCE 6400x4000 fp64, y-split (paper strong 'small', P:1407)"),
+                  label="2-D Euler FORCE 6400x4000 fp64, y-split (paper strong 'small', P:1407)",
+                  paper={"hardware": "8x V100-SXM2 16 GB (AWS p3, P:1130-1141)", "steps": 1000,
+                         "speedup_8": 6.92, "efficiency_8_stated": 0.875,
+                         "efficiency_8_from_speedup": 6.92 / 8,
+                         "cite": "P:1404-1414 (sec. 8.2); formula P:1382"}),
     "p9600": dict(ndim=2, n=(9600, 6000), dtype="f64", scaling="strong",
-                  label="2-D Euler FORCE 9600x6000 fp64, y-split (paper strong 'large', P:1408)"),
+                  label="2-D Euler FORCE 9600x6000 fp64, y-split (paper strong 'large', P:1408)",
+                  paper={"hardware": "8x V100-SXM2 16 GB (AWS p3, P:1130-1141)", "steps": 1000,
+                         "speedup_8": 7.32, "efficiency_8_stated": 0.915,
+                         "efficiency_8_from_speedup": 7.32 / 8,
+                         "cite": "P:1404-1414 (sec. 8.2); formula P:1382"}),
     "pweak": dict(ndim=2, n=(2560, 2500), dtype="f64", scaling="weak",
-                  label="2-D Euler FORCE 6.4M cells/GPU fp64, y-split (paper weak, P:1393-1402)"),
+                  label="2-D Euler FORCE 6.4M cells/GPU fp64, y-split (paper weak, P:1393-1402)",
+                  paper={"hardware": "8x V100-SXM2 16 GB (AWS p3, P:1130-1141)", "steps": 1000,
+                         "weak_efficiency_8": "around 0.95",
+                         "cite": "P:1399-1402, P:1503 (sec. 8.1); formula P:1378"}),
     # order-2 reconstruction (MUSCL-Hancock + FORCE), configs[1] shape
     "o2_1024": dict(ndim=2, n=(1024, 1024), dtype="f64", scaling="weak", order=2,
                     label="2-D Euler SLIC (MUSCL-Hancock + FORCE, order 2) 1024x1024/GPU fp64"),
@@ -668,7 +679,8 @@ def run_workload(ctx, args, name, steps, warmup, e2e_steps, headline):
                       "wall_s": wall, "dt": dt, "S0": S0, "op": op,
                       "cfl": {"loop": args.cfl_loop, "steps_per_run": M, "cfl": 0.9}
                       if op == "cfl" else None,
-                      "paper_v100_ms": wl.get("paper_ms")},
+                      "paper_v100_ms": wl.get("paper_ms"),
+                      "paper_context": wl.get("paper")},
            "roofline": roof, "gpu_launches": launches_per_step * steps,
            "halo": halo, "clocks": clk.summary()}
     if e2e:

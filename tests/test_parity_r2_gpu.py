@@ -154,3 +154,30 @@ def test_order2_3d_100_steps():
         dom.advance(dt, 100)
         Ug = dom.get_state()
     assert relerr(Ug, _orc2(U0, dt, 100, dx)) <= 1e-10
+
+
+def test_p6400_y_split_tiling_sampled_parity():
+    """f4 (the paper's strong-scaling 'small' problem) in the 8-GPU y-split
+    tiling (8 partitions of 6400x500 on one GPU): bitwise equal to one partition, and
+    sampled patches (domain corners, the partition seams, the shock, the bubble) vs
+    the oracle after 3 steps."""
+    from test_parity_gpu import _patch_oracle
+    n = (6400, 4000)
+    dx = [1.0 / 6400] * 2
+    U0 = W.shock_bubble(n, dx=dx)
+    dt = 0.4 * dx[0] / 5.8
+    k = 3
+    with R.Domain(n, dx=dx, parts=(1, 8)) as dom:
+        dom.set_state(U0)
+        dom.advance(dt, k)
+        Ug = dom.get_state()
+    with R.Domain(n, dx=dx) as dom:
+        dom.set_state(U0)
+        dom.advance(dt, k)
+        assert np.array_equal(dom.get_state(), Ug)
+    boxes = [(0, 0), (6400 - 40, 4000 - 40), (620, 480), (620, 1980), (2540, 1980),
+             (3000, 990), (6000, 3490), (0, 1480)]
+    for lo in boxes:
+        hi = (lo[0] + 40, lo[1] + 40)
+        ref, gsl = _patch_oracle(U0, lo, hi, n, k, dt, dx, "clamp")
+        assert relerr(Ug[gsl], ref) <= 1e-12, lo
