@@ -616,10 +616,19 @@ void launch_sweep(const KArgs<T>& a, int d, cudaStream_t s) {
 
 
 int auto_rows_3d(const Geom& g) {
-  // z-planes per CTA: 8-10 z-chunks (about 24 CTAs per SM), at least 16 planes per
-  // march (each chunk recomputes 2 planes).  Measured (profiles/r1/rows_sweep.txt):
-  // 384^3 fp32 39 planes 1088 us vs 128 planes 1270 us; 512^3 fp64 64 planes
-  // 4535 us vs 256 planes 4834 us; 256^3 fp64 32 planes 705 us vs 43 planes 716 us.
+  // z-planes per CTA march.  fp32 (k_step3d_rb, two CTAs per SM): 8-10 z-chunks
+  // (about 24 CTAs per SM), at least 16 planes per march (each chunk recomputes 2
+  // planes) -- round 1, profiles/r1/rows_sweep.txt: 384^3 39 planes 1088 us vs 128
+  // planes 1270 us.  fp64 (k_step3d_sp, one CTA per SM): 5 full-length chunks and a
+  // last one a third as long, whose short CTAs fill the final wave -- round 2,
+  // profiles/r2/rows_sweep*.txt: 512^3 96 planes 3.78 ms vs 64 planes 3.90 ms, 86 and
+  // 103 planes 3.90 ms.
+  if (g.elem == 8) {
+    int64_t rows = (3 * g.S[2] + 15) / 16;
+    if (rows < 16) rows = 16;
+    if (rows > g.S[2]) rows = g.S[2];
+    return (int)rows;
+  }
   const int64_t ww = window3d(g);
   const int64_t tiles = ((g.S[0] + ww - 1) / ww) * ((g.S[1] + 13) / 14);  // (TY = 14 estimate)
   int64_t nzc = (148 * 24 + tiles - 1) / tiles;

@@ -2,10 +2,13 @@
 plan exactly as the NCCL exchange does -- pack every edge whose source partition
 is mine and destination is the peer's into one message per peer (plan order),
 send/recv, unpack -- and check that every ghost of every rank's partition equals
-the oracle's single-block ghost fill.  This covers the host logic of
-rpl_create's peer lists / message layout (runtime.cu) without a GPU; the device
-pack/unpack kernels implement the same index maps and are covered on one GPU by
-the multi-partition bitwise tests.
+the oracle's single-block ghost fill.  This checks the message
+layout the NCCL transport's peer lists use (the plan's edges in plan order, one
+message per peer) on CPU, with the host re-implementing pack and unpack.  The
+library's own device path -- shell tiles, the side stream, the batched pack
+(`k_edges`) and unpack kernels, the events -- runs on one GPU through the LOOPBACK
+transport (tests/test_loopback_gpu.py, bitwise vs one partition); only the
+ncclSend/ncclRecv calls themselves need two GPUs.
 """
 import os
 import socket
