@@ -3,16 +3,17 @@
 //   k_sweep     (K-A)  one sweep along d, one thread per cell: the paper's
 //                      update_state_x / update_state_y node (Listing 8).
 //   k_sweep2           the same with order-2 (MUSCL-Hancock) reconstruction (f3).
-//   k_step2d_pt (K-B)  all sweeps of a 2-D step in one HBM pass, TMA tiles.
+//   k_step2d_ra (K-B)  all sweeps of a 2-D step in one HBM pass, TMA tiles,
+//                      adjacent row pairs per warp.
 //   k_step2d_o2        the same with order-2 reconstruction (f3).
 //   k_fill             set_boundary + halo for every ghost of a partition.
 //   k_maxws            max |u| + c over the interior (Listing 8 set_wavespeeds +
 //                      then_reduce(Max)).
-//   k_fluxdiff[_pt]    the sec. 7.3 flux difference (Table 4; f2).
-// (Slower 2-D designs measured in round 1 -- per-warp row march, column march,
-// point-to-point hand-offs, low-register, warp march, software-pipelined -- are
-// described in DESIGN.md's tuning log; their code is in git history, commits
-// dcd05af and 289ce7f.)
+//   k_fluxdiff[_ra]    the sec. 7.3 flux difference (Table 4; f2): per cell / tiled.
+// (Slower 2-D designs measured in rounds 1 and 2 -- one row per warp, per-warp row
+// march, column march, point-to-point hand-offs, low-register, warp march,
+// software-pipelined -- are described in DESIGN.md's tuning log; their code is in
+// git history.)
 // All step kernels write the ghost images of the cells they produce (scheme.cuh),
 // so no separate boundary or halo kernel runs between steps on one rank.
 #include <cuda.h>
@@ -646,7 +647,7 @@ int auto_rows_3d(const Geom& g) {
 // scalar doubles; P = pk: packed fp32), so the y-face between them is evaluated
 // in registers together with the face below row 2w, and only row 2w+1's (U*, F_y)
 // and that lower face go through shared memory.  Same tile walk, TMA ring and
-// per-cell / per-face operations as k_step2d_pt: bitwise equal.
+// per-cell / per-face operations as the split kernel k_sweep: bitwise equal.
 // ---------------------------------------------------------------------------
 template <typename P, int NW, int MB, int NS>
 __global__ void __launch_bounds__(32 * NW, MB)

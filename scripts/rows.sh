@@ -3,8 +3,8 @@
 TAG=${1:-rows}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
-run() { name=$1; shift; timeout 900 python bench.py "$@" > $OUT/$name.json 2>>$OUT/err.log; }
-run a_2d1024
+run() { name=$1; shift; timeout 900 python bench.py --extras none "$@" > $OUT/$name.json 2>>$OUT/err.log; }
+run a_2d1024 --workload 2d1024
 run a_s512 --workload s512 --steps 5 --e2e-steps 1
 run a_w384 --workload w384 --steps 10 --e2e-steps 2
 run a_l256_f32_soa --workload l256 --dtype f32 --layout soa --steps 20 --e2e-steps 2
