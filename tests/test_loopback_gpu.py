@@ -105,3 +105,22 @@ def test_loopback_fault_hook_turns_red(monkeypatch):
     ref = run_gpu(U0, dt, 5, dx=dx)
     monkeypatch.setenv("RPL_FAULT_HALO", "1")
     assert not np.array_equal(_lb(U0, dt, 5, dx=dx, parts=(2, 3)), ref)
+
+
+@pytest.mark.parametrize("n,parts,kw", [
+    ((200,), (4,), dict(bc_lo=["periodic"], bc_hi=["periodic"])),   # 1-D: split kernel
+    ((130, 64), (2, 2), dict(pad=1)),                               # pad 1 (one ghost layer)
+    ((130, 64), (1, 4), dict(order=2)),                             # order 2 in 2-D
+    ((40, 33, 48), (1, 1, 8), dict(dtype="f32")),                   # 8 thin z-slabs
+])
+def test_loopback_more_shapes_bitwise(n, parts, kw):
+    D = len(n)
+    dx = [1.0 / n[0]] * D
+    U0 = W.random_state(n, seed=47)
+    kw = dict(kw)
+    dtype = kw.pop("dtype", "f64")
+    if dtype == "f32":
+        U0 = U0.astype(np.float32)
+    dt = 0.2 * dx[0] / 3.0
+    ref = run_gpu(U0, dt, 5, dtype=dtype, dx=dx, **kw)
+    assert bits_equal(_lb(U0, dt, 5, dtype=dtype, dx=dx, parts=parts, **kw), ref)
