@@ -91,12 +91,15 @@ typedef enum { RPL_KERNEL_FUSED = 0, RPL_KERNEL_SPLIT = 1 } rpl_kernel;
  * with the halo neighbours.  LOOPBACK (nranks == 1, prod(parts) > 1): the local
  * partitions exchange halos through the NCCL path's pack -> transfer -> unpack
  * kernels and side stream, with a device copy instead of send/recv (the single-GPU
- * test of that choreography); otherwise partitions of one rank write each other's
- * ghosts directly. */
+ * test of that choreography); LOOPBACK_NCCL does the transfer with grouped
+ * ncclSend/ncclRecv to itself over a one-rank communicator the library creates
+ * (the NCCL calls of the multi-rank path, on one GPU).  Otherwise partitions of one
+ * rank write each other's ghosts directly. */
 typedef enum {
   RPL_TRANSPORT_NCCL = 0,
   RPL_TRANSPORT_P2P = 1,
-  RPL_TRANSPORT_LOOPBACK = 2
+  RPL_TRANSPORT_LOOPBACK = 2,
+  RPL_TRANSPORT_LOOPBACK_NCCL = 3
 } rpl_transport;
 
 typedef struct {

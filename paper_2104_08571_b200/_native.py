@@ -18,7 +18,7 @@ STATUS = {0: "RPL_OK", -1: "RPL_E_INVALID_ARG", -2: "RPL_E_NOT_DIVISIBLE",
 F32, F64 = 0, 1
 SOA, AOS = 0, 1
 FUSED, SPLIT = 0, 1
-TRANSPORT_NCCL, TRANSPORT_P2P, TRANSPORT_LOOPBACK = 0, 1, 2
+TRANSPORT_NCCL, TRANSPORT_P2P, TRANSPORT_LOOPBACK, TRANSPORT_LOOPBACK_NCCL = 0, 1, 2, 3
 BC_TRANSMISSIVE, BC_PERIODIC, BC_REFLECTIVE = 0, 1, 2
 MAP_TRANSLATE, MAP_REFLECT, MAP_BROADCAST = 0, 1, 2
 

@@ -294,6 +294,7 @@ struct rpl_domain {
   // partitions of one rank through the same pack -> transfer -> unpack path, device
   // copies instead of send/recv): flat edge lists with absolute message offsets
   int xmode = 0;
+  bool loop_nccl = false;  // loopback through ncclSend/ncclRecv to self (one-rank comm)
   DevEdge* d_sedges = nullptr;
   DevEdge* d_redges = nullptr;
   int n_sedges = 0, n_redges = 0;
@@ -384,10 +385,11 @@ static rpl_status geom_of(const rpl_config* c, Geom* g) {
     return fail(RPL_E_INVALID_ARG, "nranks must be 1 or prod(parts) (one partition per rank)");
   if (c->rank < 0 || c->rank >= c->nranks) return fail(RPL_E_INVALID_ARG, "rank out of range");
   if (c->transport != RPL_TRANSPORT_NCCL && c->transport != RPL_TRANSPORT_P2P &&
-      c->transport != RPL_TRANSPORT_LOOPBACK)
+      c->transport != RPL_TRANSPORT_LOOPBACK && c->transport != RPL_TRANSPORT_LOOPBACK_NCCL)
     return fail(RPL_E_INVALID_ARG, "transport");
-  if (c->transport == RPL_TRANSPORT_LOOPBACK && c->nranks != 1)
-    return fail(RPL_E_INVALID_ARG, "LOOPBACK transport is for one rank (local partitions)");
+  if ((c->transport == RPL_TRANSPORT_LOOPBACK || c->transport == RPL_TRANSPORT_LOOPBACK_NCCL) &&
+      c->nranks != 1)
+    return fail(RPL_E_INVALID_ARG, "LOOPBACK transports are for one rank (local partitions)");
   if (c->nranks > 1 && c->transport == RPL_TRANSPORT_NCCL && !c->nccl_id)
     return fail(RPL_E_INVALID_ARG, "nccl_id required");
   if (c->nranks > 32 && c->transport == RPL_TRANSPORT_P2P)
@@ -742,21 +744,24 @@ static rpl_status create_impl(const rpl_config* c, rpl_domain* d) {
       }
     }
   }
-  d->xmode = (c->nranks > 1 && !d->p2p) ? 1
-             : (c->nranks == 1 && c->transport == RPL_TRANSPORT_LOOPBACK && g.nparts > 1) ? 2
-                                                                                         : 0;
-  if (d->xmode == 1) {
+  const bool loop = c->transport == RPL_TRANSPORT_LOOPBACK ||
+                    c->transport == RPL_TRANSPORT_LOOPBACK_NCCL;
+  d->xmode = (c->nranks > 1 && !d->p2p) ? 1 : (c->nranks == 1 && loop && g.nparts > 1) ? 2 : 0;
+  d->loop_nccl = d->xmode == 2 && c->transport == RPL_TRANSPORT_LOOPBACK_NCCL;
+  if (d->xmode == 1 || d->loop_nccl) {
     if (!g_nccl.load()) return fail(RPL_E_NCCL, "libnccl.so.2 not found (set RPL_NCCL_LIB)");
     ncclUniqueId id;
-    memcpy(&id, c->nccl_id, sizeof(id));
+    if (d->loop_nccl) NC(g_nccl.GetUniqueId(&id));  // one-rank communicator of our own
+    else memcpy(&id, c->nccl_id, sizeof(id));
+    const int nr = d->loop_nccl ? 1 : c->nranks, me = d->loop_nccl ? 0 : c->rank;
     if (g_nccl.CommInitRankConfig) {
       // cap NCCL's CTAs: the interior step kernel keeps the SMs while halos move
       ncclConfig_t cc = NCCL_CONFIG_INITIALIZER;
       const char* m = getenv("RPL_NCCL_MAX_CTAS");
       cc.maxCTAs = m ? atoi(m) : 8;
-      NC(g_nccl.CommInitRankConfig(&d->comm, c->nranks, id, c->rank, &cc));
+      NC(g_nccl.CommInitRankConfig(&d->comm, nr, id, me, &cc));
     } else {
-      NC(g_nccl.CommInitRank(&d->comm, c->nranks, id, c->rank));
+      NC(g_nccl.CommInitRank(&d->comm, nr, id, me));
     }
   }
   if (d->xmode) {
@@ -960,6 +965,13 @@ static rpl_status exchange_t(rpl_domain* d, int b, cudaStream_t st) {
       NC(g_nccl.Send((T*)d->d_send + P.offset, P.elems, ty, P.rank, d->comm, st));
     for (auto& P : d->recv_peers)
       NC(g_nccl.Recv((T*)d->d_recv + P.offset, P.elems, ty, P.rank, d->comm, st));
+    NC(g_nccl.GroupEnd());
+  } else if (d->loop_nccl && d->n_selems) {
+    // the same grouped calls, to ourselves on the one-rank communicator
+    const ncclDataType_t ty = g.elem == 8 ? ncclFloat64 : ncclFloat32;
+    NC(g_nccl.GroupStart());
+    NC(g_nccl.Send((T*)d->d_send, d->n_selems, ty, 0, d->comm, st));
+    NC(g_nccl.Recv((T*)d->d_recv, d->n_relems, ty, 0, d->comm, st));
     NC(g_nccl.GroupEnd());
   } else if (d->n_selems) {
     CU(cudaMemcpyAsync(d->d_recv, d->d_send, d->n_selems * g.elem, cudaMemcpyDeviceToDevice, st));

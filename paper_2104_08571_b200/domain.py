@@ -58,7 +58,8 @@ def make_config(size, pad=2, parts=None, dtype="f64", layout="soa", kernel="fuse
     cfg.arena = int(arena) if arena else None
     cfg.rows_per_chunk = int(rows_per_chunk)
     cfg.transport = {"nccl": N.TRANSPORT_NCCL, "p2p": N.TRANSPORT_P2P,
-                     "loopback": N.TRANSPORT_LOOPBACK}[transport]
+                     "loopback": N.TRANSPORT_LOOPBACK,
+                     "loopback_nccl": N.TRANSPORT_LOOPBACK_NCCL}[transport]
     cfg.order = int(order)
     return cfg
 

@@ -52,6 +52,7 @@ def test_config_errors(kw, status):
 def test_config_ok_and_arena():
     R.config_check(size=(1024, 1024), pad=2)
     R.config_check(size=(64, 64), parts=(2, 2), transport="loopback")
+    R.config_check(size=(64, 64), parts=(2, 2), transport="loopback_nccl")
     n = R.arena_bytes(size=(1024, 1024), pad=2, dtype="f64")
     # two padded buffers, C=4 comps, pitch >= 1024 + ghosts, rows 1028
     assert 2 * 4 * 1028 * 1030 * 8 <= n <= 2 * 4 * 1028 * 1152 * 8 + 4096

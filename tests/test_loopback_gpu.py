@@ -124,3 +124,25 @@ def test_loopback_more_shapes_bitwise(n, parts, kw):
     dt = 0.2 * dx[0] / 3.0
     ref = run_gpu(U0, dt, 5, dtype=dtype, dx=dx, **kw)
     assert bits_equal(_lb(U0, dt, 5, dtype=dtype, dx=dx, parts=parts, **kw), ref)
+
+
+@pytest.mark.parametrize("n,parts,kw", [
+    ((190, 126), (2, 3), {}),                       # 2-D, overlapped (shell / side stream)
+    ((64, 32, 24), (2, 2, 2), dict(dtype="f32")),   # 3-D blocks, overlapped
+    ((64, 40, 24), (1, 2, 2), dict(order=2)),       # order 2: exchange after the step
+])
+def test_loopback_nccl_send_recv_bitwise(n, parts, kw):
+    """RPL_TRANSPORT_LOOPBACK_NCCL: the halo messages travel through grouped
+    ncclSend/ncclRecv to self on a one-rank communicator (maxCTAs config) -- the NCCL
+    calls of the multi-rank transport, on one GPU -- bitwise equal to one partition."""
+    D = len(n)
+    dx = [1.0 / n[0]] * D
+    U0 = W.shock_bubble(n, dx=dx)
+    kw = dict(kw)
+    dtype = kw.pop("dtype", "f64")
+    if dtype == "f32":
+        U0 = U0.astype(np.float32)
+    dt = 0.4 * dx[0] / 5.8
+    ref = run_gpu(U0, dt, 5, dtype=dtype, dx=dx, **kw)
+    got = run_gpu(U0, dt, 5, dtype=dtype, dx=dx, parts=parts, transport="loopback_nccl", **kw)
+    assert bits_equal(got, ref)
