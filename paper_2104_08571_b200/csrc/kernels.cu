@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(256) k_sweep2(const __grid_constant__ KArgs<T>
   if (ws) publish_max(a, wmax);
 }
 
-constexpr int kRows2 = 16;  // 2-D order-1 tile rows (box), 14 outputs
+constexpr int kRows2 = 24;  // 2-D order-1 tile rows (box), 22 outputs
 
 // TMA tile load (cp.async.bulk.tensor.4d, mbarrier completion) used by the
 // persistent 2-D kernels: box [rows][C comps][32+AL slots] of a SoA buffer.
@@ -841,15 +841,15 @@ static void launch_ra2d(const KArgs<typename PairElem<P>::T>& a, const void* tma
              *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
 }
 
-// 2-D order-1 kernel: adjacent row pairs (k_step2d_ra), 16-row tiles of 8 warps, 3
-// CTAs/SM at every partition size measured (round 1: 1024^2 26.9 us; 12-row tiles x 4
-// CTAs 27.2 us; the one-row-per-warp form 29.1 us; 6400x4000 396 us vs 24-row tiles x 1
-// CTA 415 us, 32-row 404 us -- profiles/r1/tile_shape_2d.txt, ra2d_variants.txt).
+// 2-D order-1 kernel: adjacent row pairs (k_step2d_ra), 24-row tiles (22 outputs) of
+// 12 warps, 2 CTAs/SM, 80 registers: round 2, profiles/r2/variants_2d_tiles.txt --
+// 6400x4000 402 -> 384 us, 9600x6000 884 -> 847 us, 1024^2 27.0 / 27.1 us against the
+// round-1 16-row tiles of 8 warps x 3 CTAs (a 3-stage ring: slower).
 template <typename T>
 void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   if (a.order == 2) return launch_step2d_o2<T>(a, tmap, s);
   using P = typename std::conditional<sizeof(T) == 8, pd, pk>::type;
-  launch_ra2d<P, kRows2 / 2, 3, 2>(a, tmap, s);
+  launch_ra2d<P, kRows2 / 2, 2, 2>(a, tmap, s);
 }
 
 template <typename T>

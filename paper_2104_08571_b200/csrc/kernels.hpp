@@ -9,10 +9,11 @@ namespace rpl {
 template <typename T>
 struct KArgs;
 
-// Tile of the fused order-1 step kernels: 30 output cells in x (32-lane windows), 14
-// output rows in y (8 warps x 2 rows, 16-row boxes), in 3-D a chunk of `rows` planes.
-// Tile t = (tz * ny + ty) * nx + tx; tile lists (KArgs::tiles) use this numbering.
-constexpr int kTileX = 30, kTileY = 14;
+// Tile of the fused order-1 step kernels: 30 output cells in x (32-lane windows); in
+// y 22 output rows in 2-D (12 warps x 2 rows, 24-row boxes) and 14 in 3-D (8 warps x
+// 2 rows, 16-row boxes); in 3-D a chunk of `rows` planes.  Tile t = (tz * ny + ty) * nx
+// + tx; tile lists (KArgs::tiles) use this numbering.
+constexpr int kTileX = 30, kTileY2 = 22, kTileY3 = 14;
 
 template <typename T>
 void launch_sweep(const KArgs<T>& a, int d, cudaStream_t s);      // K-A, one launch

@@ -587,7 +587,7 @@ static rpl_status setup_exchange(rpl_domain* d) {
   CU(cudaEventCreateWithFlags(&d->ev_halo, cudaEventDisableTiming));
   // shell / interior tiles of the fused order-1 kernels (2-D SoA, 3-D)
   if (g.D >= 2 && c->order == 1 && (g.D == 3 || g.layout == 0)) {
-    const int64_t wx = kTileX, wy = kTileY, wz = g.D == 3 ? d->rows : 1;
+    const int64_t wx = kTileX, wy = g.D == 3 ? kTileY3 : kTileY2, wz = g.D == 3 ? d->rows : 1;
     const int64_t nx = (g.S[0] + wx - 1) / wx, ny = (g.S[1] + wy - 1) / wy,
                   nz = g.D == 3 ? (g.S[2] + wz - 1) / wz : 1;
     std::vector<int> all;
