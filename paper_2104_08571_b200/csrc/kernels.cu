@@ -844,7 +844,9 @@ static void launch_ra2d(const KArgs<typename PairElem<P>::T>& a, const void* tma
 // 2-D order-1 kernel: adjacent row pairs (k_step2d_ra), 24-row tiles (22 outputs) of
 // 12 warps, 2 CTAs/SM, 80 registers: round 2, profiles/r2/variants_2d_tiles.txt --
 // 6400x4000 402 -> 384 us, 9600x6000 884 -> 847 us, 1024^2 27.0 / 27.1 us against the
-// round-1 16-row tiles of 8 warps x 3 CTAs (a 3-stage ring: slower).
+// round-1 16-row tiles of 8 warps x 3 CTAs (a 3-stage ring: slower); 14 warps x 2
+// (72 registers) 398 / 1007 us, 10 warps x 2 418 / 919 us, 20 warps x 1 413 / 949 us
+// (profiles/r2/variants_2d_tiles2.txt).
 template <typename T>
 void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   if (a.order == 2) return launch_step2d_o2<T>(a, tmap, s);
