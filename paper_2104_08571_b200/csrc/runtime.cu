@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing without a tool attached
+
 #include "../../include/ripple_fv.h"
 #include "geometry.hpp"
 #include "kernels.hpp"
@@ -47,6 +49,13 @@ static rpl_status fail(rpl_status st, const char* fmt, ...) {
 extern "C" const char* rpl_last_error(void) { return g_err.c_str(); }
 
 // ------------------------------------------------------------------ NCCL (dlopen)
+// NVTX range for profilers (Nsight Systems / ncu --nvtx): library calls, steps,
+// halo exchanges.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 // NCCL is resolved at run time from the libnccl.so.2 already loaded in the
 // process (torch's), else from the loader path: the library has no link-time
 // NCCL dependency and single-rank use never touches it.
@@ -902,6 +911,7 @@ static rpl_status check_flag(rpl_domain* d) {
 }
 
 extern "C" rpl_status rpl_set_state(rpl_domain* d, const void* host) {
+  NvtxRange nvtx_("rpl_set_state");
   if (!d || !host) return fail(RPL_E_INVALID_ARG, "null argument");
   CU(cudaSetDevice(d->device));
   rpl_status st = xfer(d, (void*)host, true);
@@ -920,6 +930,7 @@ extern "C" rpl_status rpl_set_state(rpl_domain* d, const void* host) {
 }
 
 extern "C" rpl_status rpl_get_state(rpl_domain* d, void* host) {
+  NvtxRange nvtx_("rpl_get_state");
   if (!d || !host) return fail(RPL_E_INVALID_ARG, "null argument");
   CU(cudaSetDevice(d->device));
   rpl_status st = xfer(d, host, false);
@@ -1087,6 +1098,7 @@ static void inject_fault(rpl_domain* d, int b) {
 }
 
 static rpl_status exchange(rpl_domain* d, int b) {
+  NvtxRange nvtx_("halo exchange");
   if (d->p2p) return p2p_sync(d, 0);  // halos were stored by the step kernel itself
   if (!d->xmode) return RPL_OK;       // one partition, or partitions writing each other's ghosts
   return d->g.elem == 8 ? exchange_t<double>(d, b, d->stream) : exchange_t<float>(d, b, d->stream);
@@ -1107,6 +1119,7 @@ static rpl_status fill_t(rpl_domain* d) {
 }
 
 extern "C" rpl_status rpl_fill_padding(rpl_domain* d) {
+  NvtxRange nvtx_("rpl_fill_padding");
   if (!d) return fail(RPL_E_INVALID_ARG, "null domain");
   CU(cudaSetDevice(d->device));
   rpl_status st = d->g.elem == 8 ? fill_t<double>(d) : fill_t<float>(d);
@@ -1198,6 +1211,7 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps, const CflArgs*
     }
   };
   for (int s = 0; s < nsteps; ++s) {
+    NvtxRange nvtx_step("step");
     const int nsweep = passes(d);
     if (cf) a.cf.step = cf->step + s;
     for (int sw = 0; sw < nsweep; ++sw) {
@@ -1213,8 +1227,11 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps, const CflArgs*
         CU(cudaGetLastError());
         CU(cudaEventRecord(d->ev_shell, d->stream));
         CU(cudaStreamWaitEvent(d->xstream, d->ev_shell, 0));
-        st = d->g.elem == 8 ? exchange_t<double>(d, nb, d->xstream)
-                            : exchange_t<float>(d, nb, d->xstream);
+        {
+          NvtxRange nvtx_x("halo exchange (side stream)");
+          st = d->g.elem == 8 ? exchange_t<double>(d, nb, d->xstream)
+                              : exchange_t<float>(d, nb, d->xstream);
+        }
         if (st) return st;
         if (hprof) cudaEventRecord(d->evh[d->evh_used + 1], d->xstream);  // halo ready
         CU(cudaEventRecord(d->ev_halo, d->xstream));
@@ -1256,6 +1273,7 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps, const CflArgs*
 }
 
 extern "C" rpl_status rpl_advance(rpl_domain* d, double dt, int32_t nsteps) {
+  NvtxRange nvtx_("rpl_advance");
   if (!d) return fail(RPL_E_INVALID_ARG, "null domain");
   if (!(dt > 0.0) || nsteps < 0) return fail(RPL_E_INVALID_ARG, "dt must be > 0, nsteps >= 0");
   CU(cudaSetDevice(d->device));
@@ -1267,6 +1285,7 @@ extern "C" rpl_status rpl_advance(rpl_domain* d, double dt, int32_t nsteps) {
 }
 
 extern "C" rpl_status rpl_max_wavespeed(rpl_domain* d, double* out) {
+  NvtxRange nvtx_("rpl_max_wavespeed");
   if (!d || !out) return fail(RPL_E_INVALID_ARG, "null argument");
   CU(cudaSetDevice(d->device));
   CU(cudaMemsetAsync(d->d_smax, 0, sizeof(unsigned long long), d->stream));
@@ -1567,6 +1586,7 @@ static rpl_status fluxdiff_t(rpl_domain* d, double dt) {
 }
 
 extern "C" rpl_status rpl_flux_difference(rpl_domain* d, double dt) {
+  NvtxRange nvtx_("rpl_flux_difference");
   if (!d) return fail(RPL_E_INVALID_ARG, "null domain");
   if (!(dt > 0.0)) return fail(RPL_E_INVALID_ARG, "dt must be > 0");
   CU(cudaSetDevice(d->device));
