@@ -9,7 +9,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libripple_fv.so")
+# RPL_LIB: another build of the library (A/B comparisons of kernel forms on one box)
+LIB_PATH = os.environ.get("RPL_LIB") or os.path.join(HERE, "libripple_fv.so")
 
 RPL_OK = 0
 STATUS = {0: "RPL_OK", -1: "RPL_E_INVALID_ARG", -2: "RPL_E_NOT_DIVISIBLE",

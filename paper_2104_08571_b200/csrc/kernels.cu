@@ -79,18 +79,18 @@ __global__ void __launch_bounds__(256) k_sweep(const __grid_constant__ KArgs<T> 
     const int64_t y = (i / g.S[0]) % g.S[1];
     const int64_t z = i / (g.S[0] * g.S[1]);
     const int64_t dm[3] = {d == 0 ? 1 : 0, d == 1 ? 1 : 0, d == 2 ? 1 : 0};
-    T Um[C], U0[C], Up[C], Fm[C], F0[C], Fp[C];
+    T Um[C], U0[C], Up[C], Am[C], Bm[C], A0[C], B0[C], Ap[C], Bp[C];
     load_cell<D, L>(g, a.in, x - dm[0], y - dm[1], z - dm[2], Um);
     load_cell<D, L>(g, a.in, x, y, z, U0);
     load_cell<D, L>(g, a.in, x + dm[0], y + dm[1], z + dm[2], Up);
-    phys_flux<D, d>(Um, Fm, a.gm1);
-    bad |= phys_flux<D, d>(U0, F0, a.gm1);
-    phys_flux<D, d>(Up, Fp, a.gm1);
+    cell_ab<D, d>(Um, Am, Bm, k.lam[d], a.gm1);
+    bad |= dom_word(U0[0], cell_ab<D, d>(U0, A0, B0, k.lam[d], a.gm1));
+    cell_ab<D, d>(Up, Ap, Bp, k.lam[d], a.gm1);
     T PL[C], PR[C], o[C];
-    force_face<D, d>(Um, Fm, U0, F0, PL, k.q[d], k.nq2[d], a.gm1);
-    force_face<D, d>(U0, F0, Up, Fp, PR, k.q[d], k.nq2[d], a.gm1);
+    face_psi<D, d>(Am, B0, PL, k.lam[d], a.gm1);
+    face_psi<D, d>(A0, Bp, PR, k.lam[d], a.gm1);
 #pragma unroll
-    for (int c = 0; c < C; ++c) o[c] = U0[c] - (PR[c] - PL[c]);
+    for (int c = 0; c < C; ++c) o[c] = psi_update(U0[c], PL[c], PR[c]);
     nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
     store_cell<D, L>(g, a.out, x, y, z, o);
     if (ws) wmax = fmax(wmax, wavespeed<D>(o, a.gm1, gam));
@@ -480,9 +480,8 @@ template void launch_xy3d_o2<float>(const KArgs<float>&, const void*, cudaStream
 template void launch_xy3d_o2<double>(const KArgs<double>&, const void*, cudaStream_t);
 
 int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
-  (void)variant;
   *box_w = 32 + 16 / g.elem;  // 16-byte-aligned TMA box start (AL extra elements)
-  *box_rows = kRows2;
+  *box_rows = variant == 3 ? 16 : kRows2;
   return 1;
 }
 
@@ -658,8 +657,8 @@ __global__ void __launch_bounds__(32 * NW, MB)
   constexpr int AL = 16 / (int)sizeof(T), WB = W + AL, STAGE = R * C * WB;
   extern __shared__ __align__(1024) unsigned char smem[];
   T* stage = reinterpret_cast<T*>(smem);
-  T* xy = stage + NS * STAGE;          // (U*, F_y) of row 2w+1, per warp
-  T* fy = xy + NW * 2 * C * W;         // face below row 2w, per warp
+  T* xy = stage + NS * STAGE;          // A_y(U*) of row 2w+1, per warp
+  T* fy = xy + NW * C * W;             // face below row 2w, per warp
   uint64_t* bar = reinterpret_cast<uint64_t*>(fy + NW * C * W);
   const Geom& g = a.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -680,7 +679,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
   const bool ws = a.cf.dev != nullptr;
   const T gam = (T)a.cf.gamma;
   T wmax = T(0);
-  const P gm1(a.gm1), qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]), nqy(kc.nq2[1]);
+  const P gm1(a.gm1), lx(kc.lam[0]), ly(kc.lam[1]);
   __syncthreads();
   const int* tl = a.tiles;  // tile list (shell-first halo overlap) or nullptr: every tile
   auto issue = [&](int i) {
@@ -698,21 +697,15 @@ __global__ void __launch_bounds__(32 * NW, MB)
 #pragma unroll
     for (int k = 0; k < NS; ++k) issue(k);
   }
-  int bad = 0, nan = 0;
+  // one domain accumulator (sign bit: rho <= 0 or p <= 0 in a flux evaluation, or a
+  // NaN/Inf output) and a stateless tile index keep the loop at 80 registers
+  int bad = 0;
   const unsigned bar_a0 = smem_u32(&bar[0]);
-  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
-  const int nyb = ntiles / nwin;
-  int idx = (int)blockIdx.x, win = 0, yb = 0;
-  bool live;
-  if (tl) {
-    live = idx < ntiles;
-    if (live) win = tl[idx] % nwin, yb = tl[idx] / nwin;
-  } else {
-    win = idx % nwin, yb = idx / nwin;
-    live = yb < nyb;
-  }
+  int idx = (int)blockIdx.x;
   const int64_t cs = g.cstride;
-  for (int i = 0; live; ++i) {
+  for (int i = 0; idx < ntiles; ++i, idx += G) {
+    const int tile = tl ? tl[idx] : idx;
+    const int win = tile % nwin, yb = tile / nwin;
     const int xw = win * (W - 2) - 1;
     const int yr0 = yb * (R - 2) - 1 + j0, yr1 = yr0 + 1;
     const int xv = xw + lane;
@@ -721,59 +714,50 @@ __global__ void __launch_bounds__(32 * NW, MB)
     const int s = NS == 2 ? (i & 1) : i % NS;
     mbar_wait_u32(bar_a0 + 8 * s, (i / NS) & 1);
     // ---- X (both rows)
-    P U[C], F[C], S_[C], G_[C];
+    P S_[C], Ay[C], By[C];
     {
+      // U^n of the two rows is read from the stage twice (for A, B and again for the
+      // update) instead of being held across the x-face evaluation: 80 registers
       const int sh = ((int)g.xo + xw) % AL;
       const T* r0 = stage + s * STAGE + j0 * C * WB + sh + lane;
       const T* r1 = r0 + C * WB;
+      P A[C], Bn[C], Pnx[C];
+      {
+        P U[C], B[C];
 #pragma unroll
-      for (int c = 0; c < C; ++c) U[c] = P(r0[c * WB], r1[c * WB]);
-    }
-    {
-      const PkDom b = phys_flux<D, 0>(U, F, gm1);
-      bad |= ((in_x & (yr0 <= SY)) ? b.a : 0) | ((in_x & (yr1 <= SY)) ? b.b : 0);
-    }
-    {
-      P Un[C], Fn[C], Pnx[C];
+        for (int c = 0; c < C; ++c) U[c] = P(r0[c * WB], r1[c * WB]);
+        const PkDom b = dom_word(U[0], cell_ab<D, 0>(U, A, B, lx, gm1));
+        bad |= ((in_x & (yr0 <= SY)) ? b.a : 0) | ((in_x & (yr1 <= SY)) ? b.b : 0);
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        Un[c] = shfl_down1(U[c]);
-        Fn[c] = shfl_down1(F[c]);
+        for (int c = 0; c < C; ++c) Bn[c] = shfl_down1(B[c]);
       }
-      force_face<D, 0>(U, F, Un, Fn, Pnx, qx, nqx, gm1);
+      face_psi<D, 0>(A, Bn, Pnx, lx, gm1);
 #pragma unroll
-      for (int c = 0; c < C; ++c) S_[c] = U[c] - (Pnx[c] - shfl_up1(Pnx[c]));
+      for (int c = 0; c < C; ++c)
+        S_[c] = psi_update(P(r0[c * WB], r1[c * WB]), shfl_up1(Pnx[c]), Pnx[c]);
     }
     {
-      const PkDom b = phys_flux<D, 1>(S_, G_, gm1);
+      const PkDom b = dom_word(S_[0], cell_ab<D, 1>(S_, Ay, By, ly, gm1));
       bad |= ((out_x & (yr0 <= SY)) ? b.a : 0) | ((out_x & (yr1 <= SY)) ? b.b : 0);
     }
     {
-      T* x1 = xy + warp * 2 * C * W + lane;
+      T* x1 = xy + warp * C * W + lane;
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        x1[c * W] = S_[c].y;
-        x1[(C + c) * W] = G_[c].y;
-      }
+      for (int c = 0; c < C; ++c) x1[c * W] = Ay[c].y;
     }
+    P Py[C];
     __syncthreads();  // (A) stage s consumed; row 2w+1 published
     if (threadIdx.x == 0) {
       fence_proxy_async();
       issue(i + NS);
     }
     // ---- Y faces (2w-1 | 2w) and (2w | 2w+1), one pair evaluation
-    P Py[C];
     {
-      const T* pdn = xy + wdn * 2 * C * W + lane;
-      P SL[C], GL[C], SR[C], GR[C];
+      const T* pdn = xy + wdn * C * W + lane;
+      P AL_[C];
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        SL[c] = P(pdn[c * W], S_[c].x);
-        GL[c] = P(pdn[(C + c) * W], G_[c].x);
-        SR[c] = P(S_[c].x, S_[c].y);
-        GR[c] = P(G_[c].x, G_[c].y);
-      }
-      force_face<D, 1>(SL, GL, SR, GR, Py, qy, nqy, gm1);
+      for (int c = 0; c < C; ++c) AL_[c] = P(pdn[c * W], Ay[c].x);
+      face_psi<D, 1>(AL_, By, Py, ly, gm1);
       T* f0 = fy + warp * C * W + lane;
 #pragma unroll
       for (int c = 0; c < C; ++c) f0[c * W] = Py[c].x;
@@ -784,7 +768,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
       const T* fu = fy + wup * C * W + lane;  // face below row 2w+2
       P o[C];
 #pragma unroll
-      for (int c = 0; c < C; ++c) o[c] = S_[c] - (P(Py[c].y, fu[c * W]) - P(Py[c].x, Py[c].y));
+      for (int c = 0; c < C; ++c) o[c] = psi_update(S_[c], Py[c], P(Py[c].y, fu[c * W]));
       const bool st0 = out_x & (j0 >= 1) & (yr0 < SY);
       const bool st1 = out_x & (j1 <= R - 2) & (yr1 < SY);
       const bool xface = (xv < g.pad) | (xv >= SX - g.pad);
@@ -799,26 +783,13 @@ __global__ void __launch_bounds__(32 * NW, MB)
         T* dst = a.out + ((int64_t)((int)g.off[1] + yr) * g.rstride + (int)g.xo + xv);
 #pragma unroll
         for (int c = 0; c < C; ++c) dst[c * cs] = v[c];
-        nan = max(nan, max(naninf(v[0]), naninf(v[C - 1])));
+        bad |= (kExpMask<T> - 1) - max(naninf(v[0]), naninf(v[C - 1]));
         if (ws) wmax = fmax(wmax, wavespeed<D>(v, a.gm1, gam));
         if (xface | (yr < g.pad) | (yr >= SY - g.pad)) images<D, 0>(a, xv, yr, 0, v);
       }
     }
-    if (tl) {
-      idx += G;
-      live = idx < ntiles;
-      if (live) win = tl[idx] % nwin, yb = tl[idx] / nwin;
-    } else {
-      win += Gr;
-      yb += Gq;
-      if (win >= nwin) {
-        win -= nwin;
-        ++yb;
-      }
-      live = yb < nyb;
-    }
   }
-  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+  if (__any_sync(kFull, bad < 0) && lane == 0) atomicOr(a.flag, 1u);
   if (ws) publish_max(a, wmax);
 }
 
@@ -827,7 +798,7 @@ static void launch_ra2d(const KArgs<typename PairElem<P>::T>& a, const void* tma
                         cudaStream_t s) {
   using T = typename PairElem<P>::T;
   constexpr int W = 32, R = 2 * NW, C = 4, AL = 16 / (int)sizeof(T);
-  const size_t bytes = (size_t)(NS * R * C * (W + AL) + NW * 3 * C * W) * sizeof(T) + 64;
+  const size_t bytes = (size_t)(NS * R * C * (W + AL) + NW * 2 * C * W) * sizeof(T) + 64;
   const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((a.g.S[1] + (R - 2) - 1) / (R - 2));
   const int ntiles = a.tiles ? a.ntiles : nwin * nyb;
@@ -851,6 +822,7 @@ template <typename T>
 void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   if (a.order == 2) return launch_step2d_o2<T>(a, tmap, s);
   using P = typename std::conditional<sizeof(T) == 8, pd, pk>::type;
+  if (a.variant == 3) return launch_ra2d<P, 8, 3, 2>(a, tmap, s);  // 16-row tiles x 3 CTAs/SM
   launch_ra2d<P, kRows2 / 2, 2, 2>(a, tmap, s);
 }
 

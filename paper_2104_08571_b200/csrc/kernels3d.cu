@@ -78,7 +78,7 @@ struct SmemRB {
   static constexpr int AL = 16 / (int)sizeof(T);
   static constexpr int WB = W + AL;
   static constexpr int STAGE = R * C * WB;
-  static constexpr int XY = NW * 2 * C * W;  // (U*, F_y) of row 2w+1, per warp
+  static constexpr int XY = NW * C * W;      // A_y(U*) of row 2w+1, per warp
   static constexpr int FY = NW * C * W;      // face below row 2w, per warp
   static constexpr size_t bytes() { return (size_t)(NS * STAGE + XY + FY) * sizeof(T) + 8 * NS; }
 };
@@ -86,8 +86,8 @@ struct SmemRB {
 template <typename P>
 struct ZPlane {
   P us[5];  // U** of the previous plane
-  P fz[5];  // F_z(U**) of the previous plane
-  P ph[5];  // z-face below the previous plane
+  P az[5];  // A_z(U**) = U** + lam_z F_z(U**) of the previous plane (scheme.cuh cell_ab)
+  P ph[5];  // z-face Psi below the previous plane
 };
 
 template <int NW, int MB, int L, typename P, int NS>
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
   int dm0 = INT_MAX, dm1 = INT_MAX, nn0 = 0, nn1 = 0;
   T wmax = T(0);
   const P gm1(a.gm1);
-  const P qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]), nqy(kc.nq2[1]), qz(kc.q[2]), nqz(kc.nq2[2]);
+  const P lx(kc.lam[0]), ly(kc.lam[1]), lz(kc.lam[2]);
   const int64_t plane = g.rstride * g.P[1], cs = g.cstride;
   T* dst0 = a.out + g.row(yr0, z0 - 1) * g.rstride + (g.xo + xs) * g.xstride;
   T* dst1 = dst0 + g.rstride;
@@ -165,50 +165,41 @@ __global__ void __launch_bounds__(32 * NW, MB)
   auto body = [&](const int kz, const ZPlane<P>& zp, ZPlane<P>& zn) {
     const int s = kz % NS;
     mbar_wait(&bar[s], (kz / NS) & 1);
-    P U[C], F[C], S_[C], G[C];
+    P U[C], S_[C], Ay[C], By[C];
     {
       const T* r0 = stage + s * SM::STAGE + xoff;
       const T* r1 = r0 + C * SM::WB;
 #pragma unroll
       for (int c = 0; c < C; ++c) U[c] = P(r0[c * cst], r1[c * cst]);
     }
-    dom_min(dm0, dm1, U[0], flux_p<D, 0>(U, F, gm1));
     {
-      P Un[C], Fn[C], Pnx[C];
+      P A[C], B[C], Bn[C], Pnx[C];
+      dom_min(dm0, dm1, U[0], cell_ab<D, 0>(U, A, B, lx, gm1));
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        Un[c] = shfl_down1(U[c]);
-        Fn[c] = shfl_down1(F[c]);
-      }
-      force_face<D, 0>(U, F, Un, Fn, Pnx, qx, nqx, gm1);
+      for (int c = 0; c < C; ++c) Bn[c] = shfl_down1(B[c]);
+      face_psi<D, 0>(A, Bn, Pnx, lx, gm1);
 #pragma unroll
-      for (int c = 0; c < C; ++c) S_[c] = U[c] - (Pnx[c] - shfl_up1(Pnx[c]));
+      for (int c = 0; c < C; ++c) S_[c] = psi_update(U[c], shfl_up1(Pnx[c]), Pnx[c]);
     }
-    dom_min(dm0, dm1, S_[0], flux_p<D, 1>(S_, G, gm1));
+    dom_min(dm0, dm1, S_[0], cell_ab<D, 1>(S_, Ay, By, ly, gm1));
     {
-      T* x1 = xy + warp * 2 * C * W + lane;  // row 2w+1 for warp w+1
+      T* x1 = xy + warp * C * W + lane;  // row 2w+1 for warp w+1
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        x1[c * W] = S_[c].y;
-        x1[(C + c) * W] = G[c].y;
-      }
+      for (int c = 0; c < C; ++c) x1[c * W] = Ay[c].y;
     }
+    P Py[C];
     __syncthreads();  // (A) stage s consumed, rows 2w+1 published
     if (threadIdx.x == 0) {
       fence_proxy_async();
       issue(kz + NS);
     }
     // Y: faces (2w-1 | 2w) and (2w | 2w+1) in one pair evaluation
-    P Py[C];
     {
-      const T* pdn = xy + wdn * 2 * C * W + lane;
-      P SL[C], GL[C];
+      const T* pdn = xy + wdn * C * W + lane;
+      P AL_[C];
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        SL[c] = P(pdn[c * W], S_[c].x);
-        GL[c] = P(pdn[(C + c) * W], G[c].x);
-      }
-      force_face<D, 1>(SL, GL, S_, G, Py, qy, nqy, gm1);
+      for (int c = 0; c < C; ++c) AL_[c] = P(pdn[c * W], Ay[c].x);
+      face_psi<D, 1>(AL_, By, Py, ly, gm1);
       T* f0 = fyb + warp * C * W + lane;  // face below row 2w, for warp w-1
 #pragma unroll
       for (int c = 0; c < C; ++c) f0[c * W] = Py[c].x;
@@ -217,15 +208,16 @@ __global__ void __launch_bounds__(32 * NW, MB)
     {
       const T* fu = fyb + wup * C * W + lane;  // face below row 2w+2 (warp w+1)
 #pragma unroll
-      for (int c = 0; c < C; ++c) zn.us[c] = S_[c] - (P(Py[c].y, fu[c * W]) - Py[c]);
-      dom_min(dm0, dm1, zn.us[0], flux_p<D, 2>(zn.us, zn.fz, gm1));
+      for (int c = 0; c < C; ++c) zn.us[c] = psi_update(S_[c], Py[c], P(Py[c].y, fu[c * W]));
+      P Bz[C];
+      dom_min(dm0, dm1, zn.us[0], cell_ab<D, 2>(zn.us, zn.az, Bz, lz, gm1));
       if (kz >= 1) {
-        force_face<D, 2>(zp.us, zp.fz, zn.us, zn.fz, zn.ph, qz, nqz, gm1);
+        face_psi<D, 2>(zp.az, Bz, zn.ph, lz, gm1);
         if (kz >= 2) {
           // update and store plane z - 1
           P o[C];
 #pragma unroll
-          for (int c = 0; c < C; ++c) o[c] = zp.us[c] - (zn.ph[c] - zp.ph[c]);
+          for (int c = 0; c < C; ++c) o[c] = psi_update(zp.us[c], zp.ph[c], zn.ph[c]);
           dst0 += plane;
           dst1 += plane;
           nn0 = max(nn0, max(naninf(o[0].x), naninf(o[C - 1].x)));
@@ -373,7 +365,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
   int dm0 = INT_MAX, dm1 = INT_MAX, nn0 = 0, nn1 = 0;
   T wmax = T(0);
   const P gm1(a.gm1);
-  const P qx(kc.q[0]), nqx(kc.nq2[0]), qy(kc.q[1]), nqy(kc.nq2[1]), qz(kc.q[2]), nqz(kc.nq2[2]);
+  const P lx(kc.lam[0]), ly(kc.lam[1]), lz(kc.lam[2]);
   const int64_t plane = g.rstride * g.P[1], cs = g.cstride;
   T* dst0 = a.out + g.row(yr0, z0 - 1) * g.rstride + (g.xo + xs) * g.xstride;
   T* dst1 = dst0 + g.rstride;
@@ -383,53 +375,44 @@ __global__ void __launch_bounds__(32 * NW, MB)
   const bool out_x = (lane >= 1) & (lane <= W - 2) & (xs < SX);
   const bool st0 = out_x & (j0 >= 1) & (yr0 < SY);
   const bool st1 = out_x & (j1 <= TY) & (yr1 < SY);
-  T* const x1 = xy + warp * 2 * C * W + lane;   // row 2w+1 for warp w+1
-  const T* const pdn = xy + wdn * 2 * C * W + lane;
+  T* const x1 = xy + warp * C * W + lane;   // row 2w+1 for warp w+1
+  const T* const pdn = xy + wdn * C * W + lane;
   T* const f0 = fyb + warp * C * W + lane;      // face below row 2w, for warp w-1
   const T* const fu = fyb + wup * C * W + lane;  // face below row 2w+2 (warp w+1)
 
-  // X: stage of plane kz -> (U*, F_y(U*)) of rows 2w, 2w+1
-  auto xphase = [&](const int kz, P* S_, P* G) {
+  // X: stage of plane kz -> U* and its y half-states (A_y, B_y) of rows 2w, 2w+1
+  auto xphase = [&](const int kz, P* S_, P* Ay, P* By) {
     const int s = kz % NS;
     mbar_wait(&bar[s], (kz / NS) & 1);
-    P U[C], F[C];
+    P U[C], A[C], B[C];
     const T* r0 = stage + s * SM::STAGE + xoff;
     const T* r1 = r0 + C * SM::WB;
 #pragma unroll
     for (int c = 0; c < C; ++c) U[c] = P(r0[c * cst], r1[c * cst]);
-    dom_min(dm0, dm1, U[0], flux_p<D, 0>(U, F, gm1));
-    P Un[C], Fn[C], Pnx[C];
+    dom_min(dm0, dm1, U[0], cell_ab<D, 0>(U, A, B, lx, gm1));
+    P Bn[C], Pnx[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) {
-      Un[c] = shfl_down1(U[c]);
-      Fn[c] = shfl_down1(F[c]);
-    }
-    force_face<D, 0>(U, F, Un, Fn, Pnx, qx, nqx, gm1);
+    for (int c = 0; c < C; ++c) Bn[c] = shfl_down1(B[c]);
+    face_psi<D, 0>(A, Bn, Pnx, lx, gm1);
 #pragma unroll
-    for (int c = 0; c < C; ++c) S_[c] = U[c] - (Pnx[c] - shfl_up1(Pnx[c]));
-    dom_min(dm0, dm1, S_[0], flux_p<D, 1>(S_, G, gm1));
+    for (int c = 0; c < C; ++c) S_[c] = psi_update(U[c], shfl_up1(Pnx[c]), Pnx[c]);
+    dom_min(dm0, dm1, S_[0], cell_ab<D, 1>(S_, Ay, By, ly, gm1));
   };
-  auto publish = [&](const P* S_, const P* G) {
+  auto publish = [&](const P* Ay) {
 #pragma unroll
-    for (int c = 0; c < C; ++c) {
-      x1[c * W] = S_[c].y;
-      x1[(C + c) * W] = G[c].y;
-    }
+    for (int c = 0; c < C; ++c) x1[c * W] = Ay[c].y;
   };
   // A, TMA refill, Y faces, B
-  auto yphase = [&](const int kz, const P* S_, const P* G, P* Py) {
+  auto yphase = [&](const int kz, const P* Ay, const P* By, P* Py) {
     __syncthreads();  // (A) stage kz consumed, rows 2w+1 of plane kz published
     if (threadIdx.x == 0) {
       fence_proxy_async();
       issue(kz + NS);
     }
-    P SL[C], GL[C];
+    P AL_[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) {
-      SL[c] = P(pdn[c * W], S_[c].x);
-      GL[c] = P(pdn[(C + c) * W], G[c].x);
-    }
-    force_face<D, 1>(SL, GL, S_, G, Py, qy, nqy, gm1);
+    for (int c = 0; c < C; ++c) AL_[c] = P(pdn[c * W], Ay[c].x);
+    face_psi<D, 1>(AL_, By, Py, ly, gm1);
 #pragma unroll
     for (int c = 0; c < C; ++c) f0[c * W] = Py[c].x;
     __syncthreads();  // (B) faces published; every warp is done reading plane kz's rows
@@ -439,14 +422,15 @@ __global__ void __launch_bounds__(32 * NW, MB)
   // the steady-state block has no branch)
   auto zphase = [&](auto M, const P* S_, const P* Py, const ZPlane<P>& zp, ZPlane<P>& zn, P* o) {
 #pragma unroll
-    for (int c = 0; c < C; ++c) zn.us[c] = S_[c] - (P(Py[c].y, fu[c * W]) - Py[c]);
-    dom_min(dm0, dm1, zn.us[0], flux_p<D, 2>(zn.us, zn.fz, gm1));
+    for (int c = 0; c < C; ++c) zn.us[c] = psi_update(S_[c], Py[c], P(Py[c].y, fu[c * W]));
+    P Bz[C];
+    dom_min(dm0, dm1, zn.us[0], cell_ab<D, 2>(zn.us, zn.az, Bz, lz, gm1));
     constexpr int m = decltype(M)::value;
     if constexpr (m >= 1) {
-      force_face<D, 2>(zp.us, zp.fz, zn.us, zn.fz, zn.ph, qz, nqz, gm1);
+      face_psi<D, 2>(zp.az, Bz, zn.ph, lz, gm1);
       if constexpr (m >= 2) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) o[c] = zp.us[c] - (zn.ph[c] - zp.ph[c]);
+        for (int c = 0; c < C; ++c) o[c] = psi_update(zp.us[c], zp.ph[c], zn.ph[c]);
         dst0 += plane;
         dst1 += plane;
 #pragma unroll
@@ -500,19 +484,20 @@ __global__ void __launch_bounds__(32 * NW, MB)
       }
     }
   };
-  // one plane with the next plane's x-sweep overlapped: (Sa, Ga) -> (Sb, Gb)
-  auto full = [&](auto M, const int kz, const P* Sa, const P* Ga, P* Sb, P* Gb,
-                  const ZPlane<P>& zp, ZPlane<P>& zn) {
+  // one plane with the next plane's x-sweep overlapped: (Sa, Aa, Ba) -> (Sb, Ab, Bb)
+  auto full = [&](auto M, const int kz, const P* Sa, const P* Aa, const P* Ba, P* Sb, P* Ab,
+                  P* Bb, const ZPlane<P>& zp, ZPlane<P>& zn) {
     P Py[C], o[C];
-    yphase(kz, Sa, Ga, Py);
-    xphase(kz + 1, Sb, Gb);
+    yphase(kz, Aa, Ba, Py);
+    xphase(kz + 1, Sb, Ab, Bb);
     zphase(M, Sa, Py, zp, zn, o);
-    publish(Sb, Gb);
+    publish(Ab);
     tail(M, kz, o);
   };
-  auto last = [&](const int kz, const P* Sa, const P* Ga, const ZPlane<P>& zp, ZPlane<P>& zn) {
+  auto last = [&](const int kz, const P* Sa, const P* Aa, const P* Ba, const ZPlane<P>& zp,
+                  ZPlane<P>& zn) {
     P Py[C], o[C];
-    yphase(kz, Sa, Ga, Py);
+    yphase(kz, Aa, Ba, Py);
     zphase(std::integral_constant<int, 2>(), Sa, Py, zp, zn, o);
     tail(std::integral_constant<int, 2>(), kz, o);
   };
@@ -520,22 +505,22 @@ __global__ void __launch_bounds__(32 * NW, MB)
   using M1 = std::integral_constant<int, 1>;
   using M2 = std::integral_constant<int, 2>;
 
-  P SA[C], GA[C], SB[C], GB[C];
+  P SA[C], AA[C], BA[C], SB[C], AB[C], BB[C];
   ZPlane<P> za, zb;
-  xphase(0, SA, GA);
-  publish(SA, GA);
-  full(M0(), 0, SA, GA, SB, GB, za, zb);  // nplanes >= 3
-  full(M1(), 1, SB, GB, SA, GA, zb, za);
+  xphase(0, SA, AA, BA);
+  publish(AA);
+  full(M0(), 0, SA, AA, BA, SB, AB, BB, za, zb);  // nplanes >= 3
+  full(M1(), 1, SB, AB, BB, SA, AA, BA, zb, za);
   int kz = 2;
   for (; kz + 2 < nplanes; kz += 2) {
-    full(M2(), kz, SA, GA, SB, GB, za, zb);
-    full(M2(), kz + 1, SB, GB, SA, GA, zb, za);
+    full(M2(), kz, SA, AA, BA, SB, AB, BB, za, zb);
+    full(M2(), kz + 1, SB, AB, BB, SA, AA, BA, zb, za);
   }
   if (kz + 1 < nplanes) {
-    full(M2(), kz, SA, GA, SB, GB, za, zb);
-    last(kz + 1, SB, GB, zb, za);
+    full(M2(), kz, SA, AA, BA, SB, AB, BB, za, zb);
+    last(kz + 1, SB, AB, BB, zb, za);
   } else {
-    last(kz, SA, GA, za, zb);
+    last(kz, SA, AA, BA, za, zb);
   }
 
   const bool bad = (st0 & ((dm0 <= 0) | (nn0 >= kExpMask<T>))) |

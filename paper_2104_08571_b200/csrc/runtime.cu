@@ -1173,6 +1173,7 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps, const CflArgs*
   a.g = g;
   for (int k = 0; k < 3; ++k) {
     const double lam = k < g.D ? dt / d->cfg.dx[k] : 0.0;
+    a.lam[k] = (T)lam;
     a.q[k] = (T)(0.25 * lam);
     a.nq2[k] = (T)(-0.25 * lam * lam);
     a.h2[k] = (T)(0.5 * lam);
