@@ -646,11 +646,12 @@ def run_workload(ctx, args, name, steps, warmup, e2e_steps, headline):
             "frac_of_8TBs": achieved / 8000.0}
     if op == "step" and wl.get("order", 1) == 1:
         # the second ceiling of this path: floating-point issue.  Algorithmic FP
-        # operations per cell-step of the scheme as written in scheme.cuh (DESIGN.md
-        # 6: 2-D 132, 3-D 240, 1-D 52; no tile recompute) against the measured lane
-        # rate of tools/dp_microbench.cu (fp64 57.4, fp32 122.1 lanes/clk/SM at
-        # 1.965 GHz on 148 SMs).
-        ops = {1: 52, 2: 132, 3: 240}[D]
+        # operations per cell-step of the scheme as written in scheme.cuh (cell_ab /
+        # face_psi / psi_update, reading A1 and 6: 9D + 35 per sweep, i.e.
+        # 2-D 106, 3-D 186, 1-D 44; no tile recompute) against the measured lane rate
+        # of tools/dp_microbench.cu (fp64 57.4, fp32 122.1 lanes/clk/SM at 1.965 GHz
+        # on 148 SMs).
+        ops = {1: 44, 2: 106, 3: 186}[D]
         lanes = 57.41 if elem == 8 else 122.11
         peak_g = lanes * 148 * 1.965
         ach_g = ops * local_cells / (per_launch_ms / 1e3) / 1e9 / \

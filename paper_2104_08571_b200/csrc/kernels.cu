@@ -479,9 +479,22 @@ void launch_xy3d_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
 template void launch_xy3d_o2<float>(const KArgs<float>&, const void*, cudaStream_t);
 template void launch_xy3d_o2<double>(const KArgs<double>&, const void*, cudaStream_t);
 
+// 2-D order-1 tile rows: 24 (22 outputs, 12 warps x 2 CTAs/SM) unless one wave of those
+// CTAs covers less than one band of tiles (more x-windows than resident CTAs), where
+// 16-row tiles (8 warps x 3 CTAs/SM) are faster: 9600x6000 812 vs 935 us, while
+// 6400x4000 355 vs 360 us and 1024^2 are unchanged (profiles/r2/variants_2d_ab.txt).
+// A 3-stage ring was slower at every size (9600x6000: 1105 / 966 us).  RPL_VARIANT 3
+// forces 16 rows, any other nonzero variant 24.
+int rows2d(const Geom& g, int variant) {
+  if (variant == 3) return 16;
+  if (variant != 0) return kRows2;
+  const int nwin = (int)((g.S[0] + 29) / 30);
+  return nwin > 2 * sm_count() ? 16 : kRows2;
+}
+
 int tmap2d_box(const Geom& g, int variant, int* box_w, int* box_rows) {
   *box_w = 32 + 16 / g.elem;  // 16-byte-aligned TMA box start (AL extra elements)
-  *box_rows = variant == 3 ? 16 : kRows2;
+  *box_rows = rows2d(g, variant);
   return 1;
 }
 
@@ -822,7 +835,7 @@ template <typename T>
 void launch_step2d(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
   if (a.order == 2) return launch_step2d_o2<T>(a, tmap, s);
   using P = typename std::conditional<sizeof(T) == 8, pd, pk>::type;
-  if (a.variant == 3) return launch_ra2d<P, 8, 3, 2>(a, tmap, s);  // 16-row tiles x 3 CTAs/SM
+  if (rows2d(a.g, a.variant) == 16) return launch_ra2d<P, 8, 3, 2>(a, tmap, s);
   launch_ra2d<P, kRows2 / 2, 2, 2>(a, tmap, s);
 }
 

@@ -297,17 +297,6 @@ __global__ void __launch_bounds__(32 * NW, MB)
 // ghost images and the device-CFL wavespeed follow it behind uniform branches.
 // Same per-cell operations as k_step3d_rb (bitwise equal).
 // ------------------------------------------------------------------------
-__device__ __forceinline__ void st_if(float* p, float v, bool ok) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f32 [%0], %1;\n}" ::"l"(p),
-               "f"(v), "r"((int)ok)
-               : "memory");
-}
-__device__ __forceinline__ void st_if(double* p, double v, bool ok) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f64 [%0], %1;\n}" ::"l"(p),
-               "d"(v), "r"((int)ok)
-               : "memory");
-}
-
 template <int NW, int MB, int L, typename P, int NS>
 __global__ void __launch_bounds__(32 * NW, MB)
     k_step3d_sp(const __grid_constant__ KArgs<typename PairElem<P>::T> a,
@@ -435,8 +424,8 @@ __global__ void __launch_bounds__(32 * NW, MB)
         dst1 += plane;
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          st_if(dst0 + c * cs, o[c].x, st0);
-          st_if(dst1 + c * cs, o[c].y, st1);
+          if (st0) dst0[c * cs] = o[c].x;
+          if (st1) dst1[c * cs] = o[c].y;
         }
         nn0 = max(nn0, max(naninf(o[0].x), naninf(o[C - 1].x)));
         nn1 = max(nn1, max(naninf(o[0].y), naninf(o[C - 1].y)));
