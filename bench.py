@@ -7,13 +7,15 @@
 Metric (BASELINE.json): Gcell-updates/s = global interior cells x steps / time / 1e9,
 plus the HBM-roofline fraction of the dominant kernel.
 
-Default workload = BASELINE.json configs[1]: 2-D Euler, 1024 x 1024 cells per GPU,
-pad 2, fp64, SoA, shock-bubble initial data (workloads.shock_bubble), fixed
-dt = 0.4 dx / S0.  At N > 1 (torchrun, one process per GPU, NCCL) the grid grows
-in y (1024 x 1024N, y-split into N partitions: the paper's weak-scaling setup,
-P:1393-1402) -> "scaling": "weak".  The two 33.5 MB state buffers fit in the
-126 MB L2, so L2 is flushed (256 MiB write) between timed steps and each step is
-timed with its own CUDA events on the library's stream (flush excluded).
+Default workload = BASELINE.json configs[2] (the headline): 3-D Euler, 512^3 cells,
+fp64, SoA, shock-bubble data (workloads.shock_bubble), fixed dt = 0.4 dx / S0,
+strong scaling (z-slabs at N > 1), with configs[3] (384^3 fp32 per GPU, weak, 2-D/3-D
+blocks) and configs[1] (1024^2 fp64 per GPU, weak: the 2-D domain grows in x and y
+and is split along y, the paper's setup P:1393-1402) as extra lines with their own
+roofline.  L2 is flushed (256 MiB write + read) between timed steps and each step
+is timed with its own CUDA events on the library's stream (flush excluded).  At N > 1
+without torchrun the script relaunches itself under torch.distributed.run (one
+process per GPU).
 
 Only the --impl reference leg and the cpu_baseline object execute oracle/ (the
 plain-C CPU oracle, timed as a reported baseline, never the product path).
