@@ -485,26 +485,45 @@ def run_workload(ctx, args, name, steps, warmup, e2e_steps, headline):
     gn, parts = decomposition(wl, world)
     D = wl["ndim"]
     dx = [1.0 / wl["n"][0]] * D
-    nccl_id = None
-    if world > 1 and args.transport == "nccl":
-        torch = ctx.torch
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(R.nccl_unique_id()), dtype=torch.uint8))
-        ctx.dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().numpy().tobytes())
     op = wl.get("op", "step")
     layout = args.layout if headline else "soa"
     kernel = args.kernel if headline else "fused"
-    dom = R.Domain(gn, pad=wl.get("pad", 2), parts=parts, dtype=wl["dtype"], kernel=kernel,
-                   dx=dx, layout=layout, nranks=world, rank=rank if world > 1 else 0,
-                   nccl_id=nccl_id, device=ctx.dev, stream=ctx.stream.cuda_stream,
-                   rows_per_chunk=args.rows,
-                   transport=args.transport if world > 1 else "nccl", order=wl.get("order", 1))
-    if world > 1 and args.transport == "p2p":
+
+    def make(transport):
+        nccl_id = None
+        if world > 1 and transport == "nccl":
+            torch = ctx.torch
+            idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                idt.copy_(torch.frombuffer(bytearray(R.nccl_unique_id()), dtype=torch.uint8))
+            ctx.dist.broadcast(idt, 0)
+            nccl_id = bytes(idt.cpu().numpy().tobytes())
+        return R.Domain(gn, pad=wl.get("pad", 2), parts=parts, dtype=wl["dtype"], kernel=kernel,
+                        dx=dx, layout=layout, nranks=world, rank=rank if world > 1 else 0,
+                        nccl_id=nccl_id, device=ctx.dev, stream=ctx.stream.cuda_stream,
+                        rows_per_chunk=args.rows,
+                        transport=transport if world > 1 else "nccl", order=wl.get("order", 1))
+
+    transport = args.transport
+    dom = make(transport)
+    if world > 1 and transport == "p2p":
+        # P2P needs CUDA IPC + peer access between every pair of GPUs; if any rank cannot
+        # attach, all ranks fall back to the NCCL transport (same arithmetic, bitwise)
         blobs = [None] * world
-        ctx.dist.all_gather_object(blobs, dom.p2p_export())
-        dom.p2p_attach(blobs)
+        ok = 1
+        try:
+            ctx.dist.all_gather_object(blobs, dom.p2p_export())
+            dom.p2p_attach(blobs)
+        except Exception as e:  # noqa: BLE001 -- reported, then the collective decision
+            print(f"bench: rank {rank}: P2P attach failed ({e}); falling back to NCCL",
+                  file=sys.stderr)
+            ok = 0
+        flag = ctx.torch.tensor([ok], dtype=ctx.torch.int32, device="cuda")
+        ctx.dist.all_reduce(flag, op=ctx.dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            dom.close()
+            transport = "nccl"
+            dom = make(transport)
     box = (dom.lo, dom.hi)
     U0 = W.shock_bubble(tuple(gn), dx=dx, box=box)
     if wl["dtype"] == "f32":
@@ -674,7 +693,7 @@ def run_workload(ctx, args, name, steps, warmup, e2e_steps, headline):
            "scaling": wl["scaling"], "vs_baseline": vs, "dtype": wl["dtype"],
            "config": {"workload": wl["label"], "global_cells": gn, "parts": parts,
                       "kernel": kernel, "layout": layout,
-                      "transport": args.transport if world > 1 else None,
+                      "transport": transport if world > 1 else None,
                       "l2": "flushed between steps (256 MiB write + 256 MiB read), per-step "
                             "CUDA events" if ctx.flush is not None else "not flushed",
                       "timing": "sum of per-step CUDA events on the library stream, max over "

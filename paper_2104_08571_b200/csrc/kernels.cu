@@ -126,15 +126,17 @@ __global__ void __launch_bounds__(256) k_sweep2(const __grid_constant__ KArgs<T>
 #pragma unroll
     for (int j = 0; j < 5; ++j)
       load_cell<D, L>(g, a.in, x + (j - 2) * dm[0], y + (j - 2) * dm[1], z + (j - 2) * dm[2], U[j]);
-    T bL[3][C], FbL[3][C], bR[3][C], FbR[3][C];
+    // FORCE between the evolved values (Ubar^R_i, Ubar^L_{i+1}) through their half-states
+    // (scheme.cuh hancock_ab / face_psi, reading A1)
+    T BL[3][C], AR[3][C];
 #pragma unroll
     for (int j = 0; j < 3; ++j)
-      bad |= hancock<D, d>(U[j], U[j + 1], U[j + 2], k.h2[d], a.gm1, bL[j], FbL[j], bR[j], FbR[j]);
+      bad |= hancock_ab<D, d>(U[j], U[j + 1], U[j + 2], k.h2[d], k.lam[d], a.gm1, BL[j], AR[j]);
     T PL[C], PR[C], o[C];
-    force_face<D, d>(bR[0], FbR[0], bL[1], FbL[1], PL, k.q[d], k.nq2[d], a.gm1);
-    force_face<D, d>(bR[1], FbR[1], bL[2], FbL[2], PR, k.q[d], k.nq2[d], a.gm1);
+    face_psi<D, d>(AR[0], BL[1], PL, k.lam[d], a.gm1);
+    face_psi<D, d>(AR[1], BL[2], PR, k.lam[d], a.gm1);
 #pragma unroll
-    for (int c = 0; c < C; ++c) o[c] = U[2][c] - (PR[c] - PL[c]);
+    for (int c = 0; c < C; ++c) o[c] = psi_update(U[2][c], PL[c], PR[c]);
     nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
     store_cell<D, L>(g, a.out, x, y, z, o);
     if (ws) wmax = fmax(wmax, wavespeed<D>(o, a.gm1, gam));
@@ -167,9 +169,10 @@ __device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map, 
 //       (hancock), face l+1/2 = FORCE(Ubar^R_l, Ubar^L_{l+1}) (shuffle), update
 //       -> U* (valid on slots 2..29), published to shared memory;
 //   Y1  rows 1..NW-2: y-slopes from the rows above/below, evolved y boundary
-//       values; Ubar^R and F_y(Ubar^R) published;
-//   Y2  rows 2..NW-2: y-face between rows j-1 and j, published;
-//   upd rows 2..NW-3: U^{n+1} = U* - (Phi_{j+1/2} - Phi_{j-1/2}), store + images.
+//       values; the half-state A = Ubar^R + lam F_y(Ubar^R) published;
+//   Y2  rows 2..NW-2: y-face Psi between rows j-1 and j (face_psi with this row's
+//       B = Ubar^L - lam F_y(Ubar^L)), published;
+//   upd rows 2..NW-3: U^{n+1} = U* - 1/4 (Psi_{j+1/2} - Psi_{j-1/2}), store + images.
 // ---------------------------------------------------------------------------
 template <typename T, int NW, int C_ = 4>
 struct SmemO2 {
@@ -178,7 +181,7 @@ struct SmemO2 {
   static constexpr int WB = W + AL;
   static constexpr int STAGE = NW * C * WB;
   static constexpr int SX = NW * C * W;
-  static constexpr int BR = NW * 2 * C * W;
+  static constexpr int BR = NW * C * W;
   static constexpr int FY = NW * C * W;
   static constexpr size_t bytes() { return (size_t)(2 * STAGE + SX + BR + FY) * sizeof(T) + 64; }
 };
@@ -227,15 +230,12 @@ __global__ void __launch_bounds__(32 * NW, MB)
     issue(0);
     issue(1);
   }
-  int bad = 0, nan = 0;
+  int bad = 0;  // sign bit: domain error or NaN/Inf output (one accumulator, see k_step2d_ra)
   const bool lane_in = (lane >= 1) & (lane <= 30);   // has both x-neighbours
   const bool lane_out = (lane >= 2) & (lane <= 29);  // U* valid
-  const int Gq = G / nwin, Gr = G - (G / nwin) * nwin;
-  int win = (int)blockIdx.x % nwin, yq = (int)blockIdx.x / nwin;  // yq = z * nyb + yb
-  const int nyz = ntiles / nwin;
   const int SZ = (int)g.S[2];
-  for (int i = 0;; ++i) {
-    if (yq >= nyz) break;
+  for (int i = 0, t = (int)blockIdx.x; t < ntiles; ++i, t += G) {
+    const int win = t % nwin, yq = t / nwin;  // yq = z * nyb + yb
     const int yb = D == 2 ? yq : yq % nyb;
     const int zp = D == 2 ? 0 : yq / nyb;
     const int xw = win * (W - 4) - 2;
@@ -257,23 +257,19 @@ __global__ void __launch_bounds__(32 * NW, MB)
         Um[c] = __shfl_up_sync(kFull, U[c], 1);
         Up[c] = __shfl_down_sync(kFull, U[c], 1);
       }
-      T bL[C], FbL[C], bR[C], FbR[C];
-      const int b = hancock<D, 0>(Um, U, Up, kc.h2[0], gm1, bL, FbL, bR, FbR);
-      bad |= (lane_in & (xv >= -1) & (xv <= SX) & row_in) ? b : 0;
       T Pnx[C];
       {
-        T bLn[C], FbLn[C];
+        T A[C], B[C], Bn[C];
+        const int b = hancock_ab<D, 0>(Um, U, Up, kc.h2[0], kc.lam[0], gm1, B, A);
+        bad |= (lane_in & (xv >= -1) & (xv <= SX) & row_in) ? b : 0;
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-          bLn[c] = __shfl_down_sync(kFull, bL[c], 1);
-          FbLn[c] = __shfl_down_sync(kFull, FbL[c], 1);
-        }
-        force_face<D, 0>(bR, FbR, bLn, FbLn, Pnx, kc.q[0], kc.nq2[0], gm1);
+        for (int c = 0; c < C; ++c) Bn[c] = __shfl_down_sync(kFull, B[c], 1);
+        face_psi<D, 0>(A, Bn, Pnx, kc.lam[0], gm1);
       }
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         const T Ppv = __shfl_up_sync(kFull, Pnx[c], 1);
-        S_[c] = U[c] - (Pnx[c] - Ppv);
+        S_[c] = psi_update(U[c], Ppv, Pnx[c]);
       }
       T* xr = sx + warp * C * W + lane;
 #pragma unroll
@@ -285,35 +281,29 @@ __global__ void __launch_bounds__(32 * NW, MB)
       issue(i + 2);
     }
     // ---- Y1: evolved y boundary values of this row
-    T byL[C], FbyL[C];
+    T By[C];  // B_y of this row's evolved lower value
     if (warp >= 1 && warp <= NW - 2) {
-      T Sm[C], Sp[C], byR[C], FbyR[C];
+      T Sm[C], Sp[C], Ay[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         Sm[c] = sx[(warp - 1) * C * W + c * W + lane];
         Sp[c] = sx[(warp + 1) * C * W + c * W + lane];
       }
-      const int b = hancock<D, 1>(Sm, S_, Sp, kc.h2[1], gm1, byL, FbyL, byR, FbyR);
+      const int b = hancock_ab<D, 1>(Sm, S_, Sp, kc.h2[1], kc.lam[1], gm1, By, Ay);
       bad |= (lane_out & (xv < SX) & (yr >= -1) & (yr <= SY)) ? b : 0;
-      T* w = br + warp * 2 * C * W + lane;
+      T* w = br + warp * C * W + lane;  // A_y of the evolved upper value, for warp + 1
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        w[c * W] = byR[c];
-        w[(C + c) * W] = FbyR[c];
-      }
+      for (int c = 0; c < C; ++c) w[c * W] = Ay[c];
     }
     __syncthreads();  // (B) Ubar^R_y published
     // ---- Y2: face between rows warp-1 and warp
     T Py[C];
     if (warp >= 2 && warp <= NW - 2) {
-      T pR[C], pF[C];
-      const T* r = br + (warp - 1) * 2 * C * W + lane;
+      T pA[C];
+      const T* r = br + (warp - 1) * C * W + lane;
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        pR[c] = r[c * W];
-        pF[c] = r[(C + c) * W];
-      }
-      force_face<D, 1>(pR, pF, byL, FbyL, Py, kc.q[1], kc.nq2[1], gm1);
+      for (int c = 0; c < C; ++c) pA[c] = r[c * W];
+      face_psi<D, 1>(pA, By, Py, kc.lam[1], gm1);
       T* fw = fyb + warp * C * W + lane;
 #pragma unroll
       for (int c = 0; c < C; ++c) fw[c * W] = Py[c];
@@ -324,7 +314,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
       const T* fu = fyb + (warp + 1) * C * W + lane;
       T o[C];
 #pragma unroll
-      for (int c = 0; c < C; ++c) o[c] = S_[c] - (fu[c * W] - Py[c]);
+      for (int c = 0; c < C; ++c) o[c] = psi_update(S_[c], Py[c], fu[c * W]);
       T* dst = a.out + (g.row(yr, zp) * g.rstride + (int)g.xo + xv);
       const int64_t cs = g.cstride;
 #pragma unroll
@@ -332,20 +322,14 @@ __global__ void __launch_bounds__(32 * NW, MB)
         *dst = o[c];
         dst += cs;
       }
-      nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
+      bad |= (kExpMask<T> - 1) - max(naninf(o[0]), naninf(o[C - 1]));
       if (ws) wmax = fmax(wmax, wavespeed<D>(o, gm1, gam));
       const bool zf = D == 3 && ((zp < g.pad) | (zp >= SZ - g.pad));
       if ((yr < g.pad) | (yr >= SY - g.pad) | (xv < g.pad) | (xv >= SX - g.pad) | zf)
         images<D, 0>(a, xv, yr, zp, o);
     }
-    win += Gr;
-    yq += Gq;
-    if (win >= nwin) {
-      win -= nwin;
-      ++yq;
-    }
   }
-  if (__any_sync(kFull, bad < 0 || nan >= kExpMask<T>) && lane == 0) atomicOr(a.flag, 1u);
+  if (__any_sync(kFull, bad < 0) && lane == 0) atomicOr(a.flag, 1u);
   if (ws) publish_max(a, wmax);
 }
 
@@ -401,26 +385,26 @@ __global__ void __launch_bounds__(128, 4) k_zmarch2(const __grid_constant__ KArg
   if (!step_coef(a, k)) return;
   const bool ws = a.cf.dev != nullptr && a.cf.last;
   const T gam = (T)a.cf.gamma;
-  const T q = k.q[2], nq2 = k.nq2[2], h2 = k.h2[2], gm1 = a.gm1;
+  const T lam = k.lam[2], h2 = k.h2[2], gm1 = a.gm1;
   T wmax = T(0);
   int bad = 0, nan = 0;
   const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (col < (int64_t)SX * SY) {
     const int x = (int)(col % SX), y = (int)(col / SX);
     const int z0 = blockIdx.y * zc, z1 = min(z0 + zc, SZ);
-    T U0[C], U1[C], Um[C], bR[C], FbR[C], Pp[C];
+    T U0[C], U1[C], Um[C], AR[C], Pp[C];  // AR: half-state A of plane z's evolved upper value
     {
-      T Umm[C], bL[C], FbL[C], cR[C], FcR[C];
+      T Umm[C], B[C], Ac[C], unused[C];
       load_cell<D, 0>(g, a.in, x, y, z0 - 2, Umm);
       load_cell<D, 0>(g, a.in, x, y, z0 - 1, Um);
       load_cell<D, 0>(g, a.in, x, y, z0, U0);
       load_cell<D, 0>(g, a.in, x, y, z0 + 1, U1);
-      bad |= hancock<D, 2>(Umm, Um, U0, h2, gm1, bL, FbL, cR, FcR);   // plane z0 - 1
-      bad |= hancock<D, 2>(Um, U0, U1, h2, gm1, bL, FbL, bR, FbR);    // plane z0
-      force_face<D, 2>(cR, FcR, bL, FbL, Pp, q, nq2, gm1);           // face z0 - 1/2
+      bad |= hancock_ab<D, 2>(Umm, Um, U0, h2, lam, gm1, unused, Ac);  // plane z0 - 1
+      bad |= hancock_ab<D, 2>(Um, U0, U1, h2, lam, gm1, B, AR);        // plane z0
+      face_psi<D, 2>(Ac, B, Pp, lam, gm1);                             // face z0 - 1/2
     }
     for (int z = z0; z < z1; ++z) {
-      T U2[C], bL[C], FbL[C], nR[C], FnR[C], P[C], o[C];
+      T U2[C], B[C], nA[C], P[C], o[C];
       // L1 prefetch of the plane the next iteration loads (no registers held
       // across the iteration; hides the HBM latency behind this plane's work)
       const int dist = a.variant == 76 ? 4 : 3;  // RPL_VARIANT 75: no prefetch
@@ -431,10 +415,10 @@ __global__ void __launch_bounds__(128, 4) k_zmarch2(const __grid_constant__ KArg
           asm volatile("prefetch.global.L1 [%0];" ::"l"(pf + c * g.cstride));
       }
       load_cell<D, 0>(g, a.in, x, y, z + 2, U2);
-      bad |= hancock<D, 2>(U0, U1, U2, h2, gm1, bL, FbL, nR, FnR);  // plane z + 1
-      force_face<D, 2>(bR, FbR, bL, FbL, P, q, nq2, gm1);           // face z + 1/2
+      bad |= hancock_ab<D, 2>(U0, U1, U2, h2, lam, gm1, B, nA);  // plane z + 1
+      face_psi<D, 2>(AR, B, P, lam, gm1);                        // face z + 1/2
 #pragma unroll
-      for (int c = 0; c < C; ++c) o[c] = U0[c] - (P[c] - Pp[c]);
+      for (int c = 0; c < C; ++c) o[c] = psi_update(U0[c], Pp[c], P[c]);
       nan = max(nan, max(naninf(o[0]), naninf(o[C - 1])));
       store_cell<D, 0>(g, a.out, x, y, z, o);
       if (ws) wmax = fmax(wmax, wavespeed<D>(o, gm1, gam));
@@ -442,8 +426,7 @@ __global__ void __launch_bounds__(128, 4) k_zmarch2(const __grid_constant__ KArg
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         Pp[c] = P[c];
-        bR[c] = nR[c];
-        FbR[c] = FnR[c];
+        AR[c] = nA[c];
         U0[c] = U1[c];
         U1[c] = U2[c];
       }
@@ -903,35 +886,36 @@ __global__ void __launch_bounds__(256) k_fluxdiff(const __grid_constant__ KArgs<
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       const int64_t dx = d == 0, dy = d == 1, dz = d == 2;
-      T Um[C], Up[C], Fm[C], F0[C], Fp[C], PL[C], PR[C];
+      T Um[C], Up[C], Am[C], Bm[C], A0[C], B0[C], Ap[C], Bp[C], PL[C], PR[C];
       load_cell<D, L>(g, a.in, x - dx, y - dy, z - dz, Um);
       load_cell<D, L>(g, a.in, x + dx, y + dy, z + dz, Up);
-      const T inv_lam = T(0.25) / a.q[d];  // 1/lam: Phi = lam F_FORCE
+      const T lam = a.lam[d];
+      const T inv4l = T(0.25) / lam;  // 1/(4 lam): Psi = 4 lam F_FORCE
       if (d == 0) {
-        phys_flux<D, 0>(Um, Fm, a.gm1);
-        phys_flux<D, 0>(U0, F0, a.gm1);
-        phys_flux<D, 0>(Up, Fp, a.gm1);
-        force_face<D, 0>(Um, Fm, U0, F0, PL, a.q[0], a.nq2[0], a.gm1);
-        force_face<D, 0>(U0, F0, Up, Fp, PR, a.q[0], a.nq2[0], a.gm1);
+        cell_ab<D, 0>(Um, Am, Bm, lam, a.gm1);
+        cell_ab<D, 0>(U0, A0, B0, lam, a.gm1);
+        cell_ab<D, 0>(Up, Ap, Bp, lam, a.gm1);
+        face_psi<D, 0>(Am, B0, PL, lam, a.gm1);
+        face_psi<D, 0>(A0, Bp, PR, lam, a.gm1);
       } else if (d == 1) {
         if constexpr (D > 1) {
-          phys_flux<D, 1>(Um, Fm, a.gm1);
-          phys_flux<D, 1>(U0, F0, a.gm1);
-          phys_flux<D, 1>(Up, Fp, a.gm1);
-          force_face<D, 1>(Um, Fm, U0, F0, PL, a.q[1], a.nq2[1], a.gm1);
-          force_face<D, 1>(U0, F0, Up, Fp, PR, a.q[1], a.nq2[1], a.gm1);
+          cell_ab<D, 1>(Um, Am, Bm, lam, a.gm1);
+          cell_ab<D, 1>(U0, A0, B0, lam, a.gm1);
+          cell_ab<D, 1>(Up, Ap, Bp, lam, a.gm1);
+          face_psi<D, 1>(Am, B0, PL, lam, a.gm1);
+          face_psi<D, 1>(A0, Bp, PR, lam, a.gm1);
         }
       } else {
         if constexpr (D > 2) {
-          phys_flux<D, 2>(Um, Fm, a.gm1);
-          phys_flux<D, 2>(U0, F0, a.gm1);
-          phys_flux<D, 2>(Up, Fp, a.gm1);
-          force_face<D, 2>(Um, Fm, U0, F0, PL, a.q[2], a.nq2[2], a.gm1);
-          force_face<D, 2>(U0, F0, Up, Fp, PR, a.q[2], a.nq2[2], a.gm1);
+          cell_ab<D, 2>(Um, Am, Bm, lam, a.gm1);
+          cell_ab<D, 2>(U0, A0, B0, lam, a.gm1);
+          cell_ab<D, 2>(Up, Ap, Bp, lam, a.gm1);
+          face_psi<D, 2>(Am, B0, PL, lam, a.gm1);
+          face_psi<D, 2>(A0, Bp, PR, lam, a.gm1);
         }
       }
 #pragma unroll
-      for (int c = 0; c < C; ++c) R[c] = fma(PR[c] - PL[c], inv_lam, R[c]);
+      for (int c = 0; c < C; ++c) R[c] = fma(PR[c] - PL[c], inv4l, R[c]);
     }
     store_cell<D, L>(g, a.out, x, y, z, R);
   }
@@ -940,11 +924,12 @@ __global__ void __launch_bounds__(256) k_fluxdiff(const __grid_constant__ KArgs<
 // ---------------------------------------------------------------------------
 // f2, tiled 2-D SoA form: every face computed once.  Persistent CTAs of NW
 // warps stream [NW rows][C][32+AL] boxes (TMA, 2-stage ring); warp j owns row
-// y0 - 1 + j.  Per row: F_x, F_y of every cell; x-face l+1/2 via shuffles (the
-// lane's right face, left face from the neighbour lane); (U, F_y) published,
-// y-face between rows j-1 and j computed once and published; rows 1..NW-2 sum
-// R = (dPhi_x) / lam_x + (dPhi_y) / lam_y with exactly k_fluxdiff's operations,
-// so both kernels agree bitwise.  One read of U, one write of R per cell.
+// y0 - 1 + j.  Per row: the half-states A, B (scheme.cuh cell_ab) of every cell in x
+// and y; x-face l+1/2 via shuffles (the lane's right face from its A and the
+// neighbour's B, left face from the neighbour lane); A_y published, y-face between
+// rows j-1 and j computed once and published; rows 1..NW-2 sum
+// R = (dPsi_x) / (4 lam_x) + (dPsi_y) / (4 lam_y) with exactly k_fluxdiff's
+// operations, so both kernels agree bitwise.  One read of U, one write of R per cell.
 // ---------------------------------------------------------------------------
 template <typename T, int NW>
 struct SmemFD {
@@ -952,7 +937,7 @@ struct SmemFD {
   static constexpr int AL = 16 / (int)sizeof(T);
   static constexpr int WB = W + AL;
   static constexpr int STAGE = NW * C * WB;
-  static constexpr int UF = NW * 2 * C * W;
+  static constexpr int UF = NW * C * W;
   static constexpr int FY = NW * C * W;
   static constexpr size_t bytes() { return (size_t)(2 * STAGE + UF + FY) * sizeof(T) + 64; }
 };
@@ -967,7 +952,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
   extern __shared__ __align__(1024) unsigned char smem[];
   T* stage = reinterpret_cast<T*>(smem);
   T* uf = stage + 2 * SM::STAGE;
-  T* fyb = uf + NW * 2 * C * W;
+  T* fyb = uf + NW * C * W;
   uint64_t* bar = reinterpret_cast<uint64_t*>(fyb + NW * C * W);
   const Geom& g = a.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -976,8 +961,8 @@ __global__ void __launch_bounds__(32 * NW, MB)
   const int SX = (int)g.S[0], SY = (int)g.S[1];
   const int G = gridDim.x;
   const P gm1(a.gm1);
-  const P ilx(T(0.25) / a.q[0]), ily(T(0.25) / a.q[1]);
-  const P qx(a.q[0]), nqx(a.nq2[0]), qy(a.q[1]), nqy(a.nq2[1]);
+  const P lx(a.lam[0]), ly(a.lam[1]);
+  const P ilx(T(0.25) / a.lam[0]), ily(T(0.25) / a.lam[1]);
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -1007,7 +992,7 @@ __global__ void __launch_bounds__(32 * NW, MB)
     const int yr0 = yb * (R - 2) - 1 + j0, yr1 = yr0 + 1;
     const int s = i & 1;
     mbar_wait(&bar[s], (i >> 1) & 1);
-    P U[C], Fx[C], Fy[C], Rx[C];
+    P U[C], Ay[C], By[C], Rx[C];
     {
       const int sh = ((int)g.xo + xw) % SM::AL;
       const T* s0 = stage + s * SM::STAGE + j0 * C * SM::WB + sh + lane;
@@ -1015,26 +1000,20 @@ __global__ void __launch_bounds__(32 * NW, MB)
 #pragma unroll
       for (int c = 0; c < C; ++c) U[c] = P(s0[c * SM::WB], s1[c * SM::WB]);
     }
-    phys_flux<D, 0>(U, Fx, gm1);
-    phys_flux<D, 1>(U, Fy, gm1);
     {
-      P Un[C], Fn[C], Pnx[C];
+      P Ax[C], Bx[C], Bn[C], Pnx[C];
+      cell_ab<D, 0>(U, Ax, Bx, lx, gm1);
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        Un[c] = shfl_down1(U[c]);
-        Fn[c] = shfl_down1(Fx[c]);
-      }
-      force_face<D, 0>(U, Fx, Un, Fn, Pnx, qx, nqx, gm1);
+      for (int c = 0; c < C; ++c) Bn[c] = shfl_down1(Bx[c]);
+      face_psi<D, 0>(Ax, Bn, Pnx, lx, gm1);
 #pragma unroll
       for (int c = 0; c < C; ++c) Rx[c] = fma(Pnx[c] - shfl_up1(Pnx[c]), ilx, P(T(0)));
     }
+    cell_ab<D, 1>(U, Ay, By, ly, gm1);
     {
-      T* w1 = uf + warp * 2 * C * W + lane;  // row 2w+1 for warp w+1
+      T* w1 = uf + warp * C * W + lane;  // row 2w+1 for warp w+1
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        w1[c * W] = U[c].y;
-        w1[(C + c) * W] = Fy[c].y;
-      }
+      for (int c = 0; c < C; ++c) w1[c * W] = Ay[c].y;
     }
     __syncthreads();  // (A)
     if (threadIdx.x == 0) {
@@ -1043,16 +1022,11 @@ __global__ void __launch_bounds__(32 * NW, MB)
     }
     P Py[C];
     {
-      const T* pdn = uf + wdn * 2 * C * W + lane;
-      P UL[C], FL[C], UR[C], FR[C];
+      const T* pdn = uf + wdn * C * W + lane;
+      P AL_[C];
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        UL[c] = P(pdn[c * W], U[c].x);
-        FL[c] = P(pdn[(C + c) * W], Fy[c].x);
-        UR[c] = P(U[c].x, U[c].y);
-        FR[c] = P(Fy[c].x, Fy[c].y);
-      }
-      force_face<D, 1>(UL, FL, UR, FR, Py, qy, nqy, gm1);
+      for (int c = 0; c < C; ++c) AL_[c] = P(pdn[c * W], Ay[c].x);
+      face_psi<D, 1>(AL_, By, Py, ly, gm1);
       T* f0 = fyb + warp * C * W + lane;  // face below row 2w, for warp w-1
 #pragma unroll
       for (int c = 0; c < C; ++c) f0[c * W] = Py[c].x;
@@ -1094,7 +1068,7 @@ static void launch_fd_ra(const KArgs<typename PairElem<P>::T>& a, const void* tm
   using T = typename PairElem<P>::T;
   constexpr int W = 32, R = 2 * NW, C = 4;
   using SM = SmemFD<T, R>;
-  const size_t bytes = (size_t)(2 * SM::STAGE + NW * 3 * C * W) * sizeof(T) + 64;
+  const size_t bytes = (size_t)(2 * SM::STAGE + NW * 2 * C * W) * sizeof(T) + 64;
   const int nwin = (int)((a.g.S[0] + (W - 2) - 1) / (W - 2));
   const int nyb = (int)((a.g.S[1] + (R - 2) - 1) / (R - 2));
   const int ntiles = nwin * nyb;

@@ -2,7 +2,7 @@
 // FADD2 / FMUL2, PTX add|sub|mul|fma.rn.f32x2).
 //
 // `pk` holds one component of two cells (a register pair).  The scheme's
-// templates in scheme.cuh (phys_flux, force_face) run unchanged on it, so a
+// templates in scheme.cuh (cell_ab, face_psi, psi_update) run unchanged on it, so a
 // packed kernel performs, per lane, exactly the IEEE operations of the scalar
 // fp32 kernels -- results are bitwise identical.
 // Measured on the B200 (tools/dp_microbench.cu): FFMA2 delivers the same lane

@@ -1174,8 +1174,6 @@ static rpl_status advance_t(rpl_domain* d, double dt, int nsteps, const CflArgs*
   for (int k = 0; k < 3; ++k) {
     const double lam = k < g.D ? dt / d->cfg.dx[k] : 0.0;
     a.lam[k] = (T)lam;
-    a.q[k] = (T)(0.25 * lam);
-    a.nq2[k] = (T)(-0.25 * lam * lam);
     a.h2[k] = (T)(0.5 * lam);
   }
   a.gm1 = (T)(d->cfg.gamma - 1.0);
@@ -1557,8 +1555,7 @@ static rpl_status fluxdiff_t(rpl_domain* d, double dt) {
   a.g = g;
   for (int k = 0; k < 3; ++k) {
     const double lam = k < g.D ? dt / d->cfg.dx[k] : 1.0;
-    a.q[k] = (T)(0.25 * lam);
-    a.nq2[k] = (T)(-0.25 * lam * lam);
+    a.lam[k] = (T)lam;
   }
   a.gm1 = (T)(d->cfg.gamma - 1.0);
   a.flag = d->d_flag;
