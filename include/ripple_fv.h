@@ -280,7 +280,9 @@ rpl_status rpl_p2p_export(rpl_domain* dom, void* blob, size_t* blob_bytes);
 
 /* P2P transport, step 2 (collective): `blobs` = the blobs of all ranks in rank
  * order (e.g. all_gather through the caller's process group), each blob_bytes
- * long.  Maps every peer's buffers; halos then travel inside the step kernels. */
+ * long.  Maps every peer's buffers; halos then travel inside the step kernels.
+ * RPL_E_UNSUPPORTED when a peer's GPU is not peer-accessible from this one (the
+ * caller then recreates the domain with the NCCL transport, as bench.py does). */
 rpl_status rpl_p2p_attach(rpl_domain* dom, const void* blobs, size_t blob_bytes);
 
 /* Free everything (collective). */

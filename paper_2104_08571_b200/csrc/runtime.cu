@@ -1531,6 +1531,11 @@ extern "C" rpl_status rpl_p2p_attach(rpl_domain* d, const void* blobs, size_t bl
       continue;
     }
     void* p = nullptr;
+    if (b.device != d->device) {  // the step kernel stores into the peer's memory directly
+      int can = 0;
+      CU(cudaDeviceCanAccessPeer(&can, d->device, b.device));
+      if (!can) return fail(RPL_E_UNSUPPORTED, "no peer access between the ranks' GPUs (use NCCL)");
+    }
     if (!d->peer_arena[r]) {
       CU(cudaIpcOpenMemHandle(&p, b.h, cudaIpcMemLazyEnablePeerAccess));
       d->peer_arena[r] = p;
