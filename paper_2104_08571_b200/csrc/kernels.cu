@@ -612,25 +612,22 @@ void launch_sweep(const KArgs<T>& a, int d, cudaStream_t s) {
 
 
 int auto_rows_3d(const Geom& g) {
-  // z-planes per CTA march.  fp32 (k_step3d_rb, two CTAs per SM): 8-10 z-chunks
-  // (about 24 CTAs per SM), at least 16 planes per march (each chunk recomputes 2
-  // planes) -- round 1, profiles/r1/rows_sweep.txt: 384^3 39 planes 1088 us vs 128
-  // planes 1270 us.  fp64 (k_step3d_sp, one CTA per SM): 5 full-length chunks and a
-  // last one a third as long, whose short CTAs fill the final wave -- round 2,
-  // profiles/r2/rows_sweep*.txt: 512^3 96 planes 3.78 ms vs 64 planes 3.90 ms, 86 and
-  // 103 planes 3.90 ms.
+  // z-planes per CTA march (each chunk recomputes 2 planes).  fp64 (k_step3d_sp, one
+  // CTA per SM): 5 full-length chunks and a last one a third as long, whose short CTAs
+  // fill the final wave -- round 2, profiles/r2/rows_sweep*.txt: 512^3 96 planes
+  // 3.78 ms vs 64 planes 3.90 ms, 86 and 103 planes 3.90 ms (after the half-state
+  // FORCE: 96 planes 3.34 ms, 80 3.36, 112 3.39, 64 3.45).  fp32 (k_step3d_rb, two CTAs
+  // per SM): 20-24 planes -- after the half-state FORCE, profiles/r2/rows_sweep4.txt:
+  // 384^3 22 planes 870 us vs 26: 881, 39: 890, 64: 943; 256^3 20 planes 324 us vs
+  // 16: 330, 26: 329.
+  int64_t rows;
   if (g.elem == 8) {
-    int64_t rows = (3 * g.S[2] + 15) / 16;
-    if (rows < 16) rows = 16;
-    if (rows > g.S[2]) rows = g.S[2];
-    return (int)rows;
+    rows = (3 * g.S[2] + 15) / 16;
+  } else {
+    rows = g.S[2] / 18;
+    if (rows < 20) rows = 20;
+    if (rows > 24) rows = 24;
   }
-  const int64_t ww = window3d(g);
-  const int64_t tiles = ((g.S[0] + ww - 1) / ww) * ((g.S[1] + 13) / 14);  // (TY = 14 estimate)
-  int64_t nzc = (148 * 24 + tiles - 1) / tiles;
-  if (nzc < 8) nzc = 8;
-  if (nzc > 10) nzc = 10;
-  int64_t rows = (g.S[2] + nzc - 1) / nzc;
   if (rows < 16) rows = 16;
   if (rows > g.S[2]) rows = g.S[2];
   return (int)rows;

@@ -30,7 +30,6 @@ template <typename T>  // order 2, 3-D SoA: x/y sweeps of all planes (box {32+AL
 void launch_xy3d_o2(const KArgs<T>& a, const void* tmap, cudaStream_t s);
 template <typename T>  // order 2, 3-D SoA: the z-sweep as a per-column march
 void launch_zmarch2(const KArgs<T>& a, cudaStream_t s);  // 0 if 2-D uses TMA  // 128-byte CUtensorMap
-int window3d(const Geom& g);                                     // outputs per 3-D x-window
 template <typename T>
 void launch_fill(const Geom& g, int part, T* const* bufs, cudaStream_t s);
 template <typename T>

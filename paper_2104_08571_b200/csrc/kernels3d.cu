@@ -610,7 +610,6 @@ int make_tmap(const Geom& g, const void* buf, void* map_out, int box_w, int box_
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
-int window3d(const Geom& g) { return 30; }
 
 // Default (variant 0; round 2, profiles/r2/): fp64 k_step3d_sp (software-pipelined
 // planes, 8 warps, 1 CTA/SM, 246 registers, 3-stage ring): 512^3 4.34 -> 3.90 ms vs the
