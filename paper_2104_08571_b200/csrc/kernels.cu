@@ -1079,15 +1079,31 @@ static void launch_fd_ra(const KArgs<typename PairElem<P>::T>& a, const void* tm
       a, *reinterpret_cast<const CUtensorMap*>(tmap), nwin, ntiles);
 }
 
-int fd_tile_rows(int elem) { return 16; }
+// fp32: 24-row tiles (12 warps x 2 CTAs/SM) -- round 2, profiles/r2/variants_fd_tiles2.txt:
+// 32768^2 13.0-13.7 -> 8.3 ms, 16384^2 2.12 -> 1.97 ms, 8192^2 505 -> 497 us against the
+// 16-row tiles of 8 warps x 4 CTAs (RPL_VARIANT 4: 8 warps x 3 CTAs, 5: the old tiles).
+// fp64: 16-row tiles x 2 CTAs (RPL_VARIANT 3: 24-row tiles x 1 CTA)
+int fd_tile_rows(int elem, int variant) {
+  if (variant == 6) return 32;
+  if (elem == 4) return (variant == 4 || variant == 5) ? 16 : 24;
+  return variant == 3 ? 24 : 16;
+}
 
 template <typename T>
 void launch_fluxdiff_tiled(const KArgs<T>& a, const void* tmap, cudaStream_t s) {
-  // adjacent row pairs, 8 warps, 16-row box: fp32 packed (FFMA2) x 4 CTAs/SM, fp64
-  // double pairs x 2 CTAs/SM (round 1: fd8k fp32 561 us, fp64 991 us; the
-  // one-row-per-warp and rows-w,w+8 forms were slower -- profiles/r1/fd_*.txt)
-  if constexpr (sizeof(T) == 4) return launch_fd_ra<8, 4>(a, tmap, s);
-  else return launch_fd_ra<8, 2, pd>(a, tmap, s);
+  // adjacent row pairs: fp32 packed (FFMA2) 24-row tiles of 12 warps x 2 CTAs/SM, fp64
+  // double pairs 16-row tiles x 2 CTAs/SM (round 1: the one-row-per-warp and
+  // rows-w,w+8 forms were slower -- profiles/r1/fd_*.txt; tile shapes: fd_tile_rows)
+  if constexpr (sizeof(T) == 4) {
+    if (a.variant == 4) return launch_fd_ra<8, 3>(a, tmap, s);
+    if (a.variant == 5) return launch_fd_ra<8, 4>(a, tmap, s);
+    if (a.variant == 6) return launch_fd_ra<16, 2>(a, tmap, s);
+    return launch_fd_ra<12, 2>(a, tmap, s);
+  } else {
+    if (a.variant == 3) return launch_fd_ra<12, 1, pd>(a, tmap, s);
+    if (a.variant == 6) return launch_fd_ra<16, 1, pd>(a, tmap, s);
+    return launch_fd_ra<8, 2, pd>(a, tmap, s);
+  }
 }
 template void launch_fluxdiff_tiled<float>(const KArgs<float>&, const void*, cudaStream_t);
 template void launch_fluxdiff_tiled<double>(const KArgs<double>&, const void*, cudaStream_t);

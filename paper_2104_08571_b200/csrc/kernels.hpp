@@ -40,7 +40,7 @@ template <typename T>
 void launch_fluxdiff(const KArgs<T>& a, cudaStream_t s);  // sec. 7.3 flux difference (f2)
 template <typename T>  // tiled 2-D SoA form (TMA box {32+AL, C, fd_tile_rows, 1})
 void launch_fluxdiff_tiled(const KArgs<T>& a, const void* tmap, cudaStream_t s);
-int fd_tile_rows(int elem);
+int fd_tile_rows(int elem, int variant);
 
 int auto_rows_3d(const Geom& g);
 const char* step3d_kernel_name(int elem, int variant);  // the 3-D step kernel launch_step3d picks

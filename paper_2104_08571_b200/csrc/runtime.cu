@@ -1571,7 +1571,7 @@ static rpl_status fluxdiff_t(rpl_domain* d, double dt) {
     for (int p : d->local)
       for (int b = 0; b < 2; ++b)
         if (make_tmap(g, d->buf[b][p], d->tmap_fd[b][p].b, 32 + 16 / g.elem,
-                      fd_tile_rows(g.elem)) != 0)
+                      fd_tile_rows(g.elem, d->variant)) != 0)
           return fail(RPL_E_CUDA, "cuTensorMapEncodeTiled failed for the flux-difference kernel");
     d->fd_tmaps = true;
   }
