@@ -637,8 +637,8 @@ int auto_rows_3d(const Geom& g) {
 // ---------------------------------------------------------------------------
 // K-B (2-D), adjacent row pairs: warp w owns tile rows 2w and 2w+1 (P = pd: two
 // scalar doubles; P = pk: packed fp32), so the y-face between them is evaluated
-// in registers together with the face below row 2w, and only row 2w+1's (U*, F_y)
-// and that lower face go through shared memory.  Same tile walk, TMA ring and
+// in registers together with the face below row 2w, and only row 2w+1's half-state
+// A_y (scheme.cuh cell_ab) and that lower face go through shared memory.  Same tile walk, TMA ring and
 // per-cell / per-face operations as the split kernel k_sweep: bitwise equal.
 // ---------------------------------------------------------------------------
 template <typename P, int NW, int MB, int NS>

@@ -9,14 +9,15 @@
 //   TMA   one elected thread streams the plane tile [16 rows][C comps][32+AL] into
 //         an NS-stage shared-memory ring (cp.async.bulk.tensor.4d, mbarrier
 //         completion), NS planes ahead of the compute;
-//   X     every warp x-sweeps its two rows in registers (warp shuffles share the
-//         x-faces, each face computed once), evaluates F_y of the result and
-//         publishes row 2w+1's (U*, F_y) in shared memory;
+//   X     every warp x-sweeps its two rows in registers (half-states A, B of every
+//         cell, scheme.cuh cell_ab; one warp shuffle of B shares each x-face, which
+//         is computed once by face_psi), forms the y half-states (A_y, B_y) of the
+//         result and publishes row 2w+1's A_y in shared memory;
 //   Y     warp w computes the y-faces (2w-1|2w) and (2w|2w+1) in one pair
 //         evaluation (the second in registers) and publishes the first;
 //   Z     every warp keeps a z-march state per cell in registers (U** of the
-//         previous plane, its F_z and the previous z-face), computes the z-face,
-//         updates and stores plane z-1 (+ ghost images on partition faces).
+//         previous plane, its A_z and the previous z-face Psi), computes the
+//         z-face, updates and stores plane z-1 (+ ghost images on partition faces).
 // Two __syncthreads per plane order the shared-memory hand-offs.  HBM traffic per
 // cell-step is one read of U^n (plus the tile halo, mostly L2 hits) and one write
 // of U^{n+1}; the halo rows/planes are recomputed, not re-stored.
